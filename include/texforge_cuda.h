@@ -1,0 +1,174 @@
+/*
+ * texforge_cuda.h — C ABI of the B200-native GLCM engine (libtexforge_cuda.so).
+ *
+ * This is the drop-in boundary beneath the reference's header-only C++ API
+ * (R/ = /root/reference/proj/, namespace texforge). Every heavy reference
+ * function maps to one entry point here; the C++ shim headers in
+ * paper_1710_06189_b200/include/texforge/ and the Python mirror in
+ * paper_1710_06189_b200/texforge.py forward to these. Plain pointers and sizes
+ * only: no C++ types, no torch types, no exceptions cross this boundary.
+ *
+ * Conventions (all from the reference):
+ *  - images are u8 row-major; `pitch` >= width is the row stride in bytes;
+ *  - a GLCM is levels*levels u64, row = reference (displaced) gray, column =
+ *    anchor gray (R/include/texforge/glcm.hpp:35-39);
+ *  - (distance, angle) -> (drow, dcol): 0:(0,+d) 45:(+d,-d) 90:(+d,0)
+ *    135:(+d,+d) (glcm.hpp:71-80);
+ *  - `pixel_levels` describes the input pixels: 256 = raw 8-bit gray, quantised
+ *    on the fly as q = (v*levels)>>8 (image.hpp:55-62, fused into the vote);
+ *    == levels = an already-quantised QuantizedImage whose values must be
+ *    < levels (image.hpp:46-48; violation -> TFG_INVALID_ARGUMENT).
+ *
+ * Return codes: 0 OK; 1 invalid argument (the message text equals the
+ * reference's std::invalid_argument text where one exists); 2 CUDA error;
+ * 3 NCCL/collective error; 4 out of memory; 5 chunk-source failure (the
+ * reference's PipelineError, pipeline.hpp:25-29; tfg_last_error_chunk() holds
+ * the failing chunk index). The message is in tfg_last_error() (thread-local).
+ *
+ * Threading: every synchronous call blocks until its results are on the host.
+ * A context serialises its own calls with a mutex; use one context per thread
+ * for concurrency. The *_async entry points only enqueue on the caller's stream.
+ */
+#ifndef TEXFORGE_CUDA_H
+#define TEXFORGE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TFG_ABI_VERSION 1
+
+enum tfg_status {
+  TFG_OK = 0,
+  TFG_INVALID_ARGUMENT = 1,
+  TFG_CUDA_ERROR = 2,
+  TFG_COLLECTIVE_ERROR = 3,
+  TFG_OUT_OF_MEMORY = 4,
+  TFG_SOURCE_ERROR = 5
+};
+
+/* flags for tfg_glcm / tfg_glcm_bands / tfg_glcm_chunked */
+enum tfg_flags {
+  TFG_INPUT_DEVICE = 1u << 0,   /* px is a device pointer (else host memory) */
+  TFG_SYMMETRIC = 1u << 1,      /* counts_out = M + M^T          (glcm.hpp:150-156) */
+  TFG_NORMALIZE = 1u << 2,      /* probs_out = normalize(counts) (glcm.hpp:167-177) */
+  TFG_FEATURES = 1u << 3,       /* feats_out = extract_features  (features.hpp:37-69) */
+  TFG_SCHEME_GLOBAL = 1u << 4,  /* Scheme 1: per-pair global atomics (ablation, parallel.hpp:121-152) */
+  TFG_SEQUENTIAL = 1u << 5      /* chunked: no copy/compute overlap (pipeline.hpp:205-208) */
+};
+
+/* Vote strategy override (testing / ablation). 0 = automatic by levels. */
+#define TFG_STRATEGY_SHIFT 16
+#define TFG_STRATEGY(s) ((unsigned)(s) << TFG_STRATEGY_SHIFT)
+enum tfg_strategy {
+  TFG_STRAT_AUTO = 0,
+  TFG_STRAT_COPIES32 = 1, /* 32 lane-interleaved u32 sub-GLCM copies per CTA (L <= 32)  */
+  TFG_STRAT_COPIES8 = 2,  /* 8 interleaved u32 copies per CTA (L <= 64)                 */
+  TFG_STRAT_COPY1 = 3,    /* one u32 copy per CTA (L <= 238)                            */
+  TFG_STRAT_PACKED16 = 4  /* one copy of packed u16 counters + exact spill (L <= 256)   */
+};
+
+typedef struct tfg_ctx tfg_ctx;
+
+/*
+ * Chunk source callback (adapts texforge::ChunkSource::fetch,
+ * R/include/texforge/pipeline.hpp:77-84). Must fill `dst` (pinned, row stride
+ * `width`) with rows [owned_row_start, buffer_row_end) of the image, pixels as
+ * described by `pixel_levels`. Return 0 on success; non-zero aborts the
+ * pipeline with TFG_SOURCE_ERROR. `err`/`err_len` receive an optional message.
+ */
+typedef int (*tfg_fetch_fn)(void* user, size_t chunk_index, size_t owned_row_start,
+                            size_t owned_row_end, size_t buffer_row_end, uint8_t* dst,
+                            char* err, size_t err_len);
+
+/* ---- context ------------------------------------------------------------ */
+int tfg_ctx_create(tfg_ctx** out, int device, unsigned flags);
+void tfg_ctx_destroy(tfg_ctx* ctx);
+const char* tfg_last_error(void);
+size_t tfg_last_error_chunk(void);
+int tfg_abi_version(void);
+/* number of engine kernels this context has launched (evidence counter) */
+uint64_t tfg_launch_count(tfg_ctx* ctx);
+
+/* ---- host-side geometry (glcm.hpp:71-104, pipeline.hpp:48-73, parallel.hpp:39-61) */
+int tfg_neighbor_offset(int distance, int angle_deg, long* drow, long* dcol);
+int tfg_valid_pair_count(size_t width, size_t height, int distance, int angle_deg, uint64_t* out);
+/* specs_out: chunk_count x {owned_row_start, owned_row_end, buffer_row_end} */
+int tfg_partition(size_t width, size_t height, int distance, int angle_deg, size_t chunk_count,
+                  uint64_t* specs_out);
+int tfg_plan(int levels, size_t scratch_budget, unsigned worker_count, unsigned* copies,
+             unsigned* groups_per_unit, int* degraded);
+
+/* ---- synthetic inputs (image.hpp:76-116), host generators, bit-identical --- */
+int tfg_synth_noise(size_t width, size_t height, uint32_t seed, uint8_t* out);
+int tfg_synth_smooth(size_t width, size_t height, uint32_t seed, uint8_t* out, int threads);
+
+/* ---- the hot path ---------------------------------------------------------- */
+
+/* quantize (image.hpp:55-62) on the device; gray/out host or device per flags */
+int tfg_quantize(tfg_ctx* ctx, const uint8_t* gray, size_t n, int levels, uint8_t* out,
+                 unsigned flags);
+
+/*
+ * One image, n_dt (distance, angle) pairs. Replaces compute_glcm_serial
+ * (glcm.hpp:144), compute_glcm_privatized (parallel.hpp:240) and, with
+ * TFG_SCHEME_GLOBAL, compute_glcm_shared (parallel.hpp:143). Host input is
+ * streamed through the K-chunk copy/compute pipeline (Scheme 3).
+ * counts_out: n_dt*L*L u64 (host). probs_out: n_dt*L*L f64 or NULL.
+ * feats_out: n_dt*5 f64 {energy, contrast, homogeneity, entropy, correlation} or NULL.
+ */
+int tfg_glcm(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t pitch,
+             int pixel_levels, int levels, const int* distances, const int* angles_deg, int n_dt,
+             unsigned flags, uint64_t* counts_out, double* probs_out, double* feats_out);
+
+/*
+ * Multispectral batch: n_bands images of width x height, band b at
+ * px + b*band_stride. counts_out: n_bands*n_dt*L*L (band-major).
+ */
+int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t pitch,
+                   size_t band_stride, size_t n_bands, int pixel_levels, int levels,
+                   const int* distances, const int* angles_deg, int n_dt, unsigned flags,
+                   uint64_t* counts_out, double* probs_out, double* feats_out);
+
+/*
+ * Scheme 3 (compute_glcm_chunked, pipeline.hpp:246-337): K row chunks from
+ * partition(), fetched by `fetch` into a pinned ring, H2D on a copy stream
+ * overlapped with voting on the exec stream into one device accumulator.
+ */
+int tfg_glcm_chunked(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, int levels,
+                     const int* distances, const int* angles_deg, int n_dt, size_t chunk_count,
+                     tfg_fetch_fn fetch, void* user, unsigned flags, uint64_t* counts_out,
+                     double* probs_out, double* feats_out);
+
+/* post-processing on the device (host in/out) */
+int tfg_symmetrize(tfg_ctx* ctx, const uint64_t* counts, int levels, uint64_t* out);
+int tfg_normalize(tfg_ctx* ctx, const uint64_t* counts, int levels, double* out);
+int tfg_features(tfg_ctx* ctx, const double* probs, int levels, double* out5);
+
+/*
+ * Device-resident asynchronous entry (no host sync): ADDS the GLCM of one
+ * (d, theta) of a device image into d_counts (L*L u64, device) on `stream`
+ * (a cudaStream_t; NULL = the context's exec stream). `row_end` limits the
+ * anchor rows (the owned rows of a shard; pass height for the whole image):
+ * rows [row_end, height) are read-only halo, exactly like a ChunkSpec.
+ * Used by the benchmark, the multi-GPU row shards and the parity tests.
+ */
+int tfg_glcm_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t height, size_t pitch,
+                   size_t row_end, int pixel_levels, int levels, int distance, int angle_deg,
+                   unsigned flags, uint64_t* d_counts, void* stream);
+
+/* Device post-processing on `stream`: symmetrize (in place allowed? no: out != in). */
+int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned flags,
+                   uint64_t* d_sym_out, double* d_probs_out, double* d_feats_out, void* stream);
+
+/* Device error flag accumulated by *_async calls (non-zero = a quantised input held a
+ * value >= levels); reading it synchronises the context's streams and clears it. */
+int tfg_check_async_errors(tfg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TEXFORGE_CUDA_H */

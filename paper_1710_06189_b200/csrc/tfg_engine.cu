@@ -1,0 +1,948 @@
+// tfg_engine.cu — host side of libtexforge_cuda.so: context, kernel dispatch,
+// the Scheme-3 stream pipeline and the C ABI declared in include/texforge_cuda.h.
+//
+// Reference mapping (R/ = /root/reference/proj/):
+//   tfg_glcm          <- compute_glcm_serial / _privatized / _shared
+//                        (glcm.hpp:144, parallel.hpp:240, parallel.hpp:143)
+//   tfg_glcm_chunked  <- compute_glcm_chunked (pipeline.hpp:246-337)
+//   tfg_glcm_bands    <- a loop of single-image calls in the reference
+//   tfg_symmetrize / tfg_normalize / tfg_features <- glcm.hpp:150-177, features.hpp:37-69
+//   tfg_quantize      <- quantize (image.hpp:55-62)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/texforge_cuda.h"
+#include "tfg_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_error;
+thread_local size_t g_error_chunk = 0;
+
+struct Failure {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Failure{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) fail(TFG_OUT_OF_MEMORY, std::string(what) + ": out of device memory");
+  fail(TFG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TFG_OK;
+  } catch (const Failure& e) {
+    g_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_error = "host out of memory";
+    return TFG_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return TFG_CUDA_ERROR;
+  }
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes <= cap) return p;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    cap = bytes;
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes <= cap) return p;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    ck(cudaMallocHost(&p, bytes), "cudaMallocHost");
+    cap = bytes;
+    return p;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct tfg_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t exec = nullptr, copy = nullptr;
+  static constexpr int kSlots = 3;
+  DevBuf dslot[kSlots];                  // device chunk ring
+  HostBuf hslot[kSlots];                 // pinned chunk ring (chunk sources)
+  cudaEvent_t copied[kSlots]{}, consumed[kSlots]{};
+  DevBuf img;                            // aligned copy of a device/host image
+  DevBuf acc;                            // u64 accumulators
+  DevBuf sym, probs, feats;              // post-processing outputs
+  DevBuf partials;                       // per-CTA sub-GLCMs (large L)
+  DevBuf qbuf;                           // quantize in/out
+  DevBuf tmp;                            // per-(d,theta) band scratch
+  int* d_err = nullptr;                  // async error flag (+ per-GLCM flags)
+  DevBuf errs;
+  HostBuf hout;                          // pinned result staging
+  std::atomic<uint64_t> launches{0};
+  std::mutex mu;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void check_levels(int levels, const char* who) {
+  if (levels < 2 || levels > 256) fail(TFG_INVALID_ARGUMENT, std::string(who) + ": levels must be in [2, 256]");
+}
+
+// glcm.hpp:71-80
+bool offset_of(int distance, int angle, long* dr, long* dc) {
+  switch (angle) {
+    case 0: *dr = 0; *dc = distance; return true;
+    case 45: *dr = distance; *dc = -distance; return true;
+    case 90: *dr = distance; *dc = 0; return true;
+    case 135: *dr = distance; *dc = distance; return true;
+    default: return false;
+  }
+}
+
+void check_angle(int angle) {
+  long a, b;
+  if (!offset_of(1, angle, &a, &b)) fail(TFG_INVALID_ARGUMENT, "angle must be one of 0, 45, 90, 135");
+}
+
+// glcm.hpp:98-104 (check_glcm_inputs)
+void check_geometry(size_t width, size_t height, int distance) {
+  const size_t d = (size_t)distance;
+  if (distance < 1 || d >= width || d >= height)
+    fail(TFG_INVALID_ARGUMENT, "glcm: degenerate geometry (d must be in [1, min(width, height)))");
+}
+
+int pick_strategy(int levels, unsigned flags) {
+  const int forced = (int)((flags >> TFG_STRATEGY_SHIFT) & 0xF);
+  const size_t cells = (size_t)levels * levels;
+  if (forced) {
+    const bool ok = (forced == TFG_STRAT_COPIES32 && cells * 128 <= 227 * 1024) ||
+                    (forced == TFG_STRAT_COPIES8 && cells * 32 <= 227 * 1024) ||
+                    (forced == TFG_STRAT_COPY1 && cells * 4 <= 227 * 1024) ||
+                    (forced == TFG_STRAT_PACKED16);
+    if (!ok) fail(TFG_INVALID_ARGUMENT, "strategy does not fit shared memory for these levels");
+    return forced;
+  }
+  if (levels <= 32) return tfg::S_COPIES32;
+  if (levels <= 64) return tfg::S_COPIES8;
+  if (cells * 4 <= 227 * 1024) return tfg::S_COPY1;
+  return tfg::S_PACKED16;
+}
+
+size_t hist_words_of(int strat, int levels) {
+  const size_t cells = (size_t)levels * levels;
+  size_t w = 0;
+  switch (strat) {
+    case tfg::S_COPIES32: w = cells * 32; break;
+    case tfg::S_COPIES8: w = cells * 8; break;
+    case tfg::S_COPY1: w = cells; break;
+    default: w = std::min<size_t>(cells, 32768); break;
+  }
+  return (w + 3) & ~size_t(3);
+}
+
+using VoteKernel = void (*)(const tfg::VoteParams);
+
+template <int Q, int S>
+VoteKernel pick_k(int ksel) {
+  switch (ksel) {
+    case 0: return tfg::glcm_vote_kernel<Q, S, 0>;
+    case 1: return tfg::glcm_vote_kernel<Q, S, 1>;
+    case 2: return tfg::glcm_vote_kernel<Q, S, 2>;
+    case 3: return tfg::glcm_vote_kernel<Q, S, 3>;
+    default: return tfg::glcm_vote_kernel<Q, S, 4>;
+  }
+}
+template <int Q>
+VoteKernel pick_s(int strat, int ksel) {
+  switch (strat) {
+    case tfg::S_COPIES32: return pick_k<Q, tfg::S_COPIES32>(ksel);
+    case tfg::S_COPIES8: return pick_k<Q, tfg::S_COPIES8>(ksel);
+    case tfg::S_COPY1: return pick_k<Q, tfg::S_COPY1>(ksel);
+    default: return pick_k<Q, tfg::S_PACKED16>(ksel);
+  }
+}
+VoteKernel pick_vote(int quant, int strat, int ksel) {
+  switch (quant) {
+    case tfg::Q_NONE: return pick_s<tfg::Q_NONE>(strat, ksel);
+    case tfg::Q_CLAMP: return pick_s<tfg::Q_CLAMP>(strat, ksel);
+    case tfg::Q_SHIFT: return pick_s<tfg::Q_SHIFT>(strat, ksel);
+    default: return pick_s<tfg::Q_MUL>(strat, ksel);
+  }
+}
+template <int Q>
+VoteKernel pick_g(int ksel) {
+  switch (ksel) {
+    case 0: return tfg::glcm_vote_global_kernel<Q, 0>;
+    case 1: return tfg::glcm_vote_global_kernel<Q, 1>;
+    case 2: return tfg::glcm_vote_global_kernel<Q, 2>;
+    case 3: return tfg::glcm_vote_global_kernel<Q, 3>;
+    default: return tfg::glcm_vote_global_kernel<Q, 4>;
+  }
+}
+VoteKernel pick_global(int quant, int ksel) {
+  switch (quant) {
+    case tfg::Q_NONE: return pick_g<tfg::Q_NONE>(ksel);
+    case tfg::Q_CLAMP: return pick_g<tfg::Q_CLAMP>(ksel);
+    case tfg::Q_SHIFT: return pick_g<tfg::Q_SHIFT>(ksel);
+    default: return pick_g<tfg::Q_MUL>(ksel);
+  }
+}
+
+struct KernelInfo {
+  VoteKernel fn = nullptr;
+  int smem_set = -1;
+  int blocks_per_sm = 0;
+};
+std::mutex g_kinfo_mu;
+std::vector<std::pair<VoteKernel, KernelInfo>> g_kinfo;
+
+int occupancy_for(VoteKernel fn, size_t smem) {
+  std::lock_guard<std::mutex> lk(g_kinfo_mu);
+  for (auto& e : g_kinfo)
+    if (e.first == fn && e.second.smem_set == (int)smem) return e.second.blocks_per_sm;
+  ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)std::max<size_t>(smem, 0)),
+     "cudaFuncSetAttribute");
+  int bps = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, reinterpret_cast<const void*>(fn), tfg::kThreads, smem),
+     "occupancy");
+  if (bps < 1) fail(TFG_CUDA_ERROR, "vote kernel cannot be resident (shared memory / registers)");
+  KernelInfo ki;
+  ki.fn = fn;
+  ki.smem_set = (int)smem;
+  ki.blocks_per_sm = bps;
+  g_kinfo.push_back({fn, ki});
+  return bps;
+}
+
+int floor_div(long a, long b) {
+  long q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+  return (int)q;
+}
+
+// Geometry of one (d, theta) vote over a buffer of `height` rows of which
+// anchor rows [0, row_end) are owned (vote_anchor_rows, glcm.hpp:110-130).
+struct VoteGeometry {
+  tfg::VoteParams p{};
+  int ksel = 4;
+  bool empty = false;
+};
+
+VoteGeometry make_geometry(size_t width, size_t height, size_t pitch, size_t row_end, int levels,
+                           int pixel_levels, int distance, int angle) {
+  VoteGeometry g;
+  long dr, dc;
+  offset_of(distance, angle, &dr, &dc);
+  const long d = distance;
+  tfg::VoteParams& p = g.p;
+  p.pitch = pitch;
+  p.levels = levels;
+  p.dr = (int)dr;
+  const long qq = floor_div(dc, 16);
+  p.qoff = (int)(qq * 16);
+  const long rem = dc - qq * 16;  // 0..15
+  g.ksel = rem == 0 ? 4 : (int)(rem >> 2);
+  p.sbits = (int)((rem & 3) * 8);
+  p.col_begin = dc < 0 ? (int)d : 0;
+  p.col_end = dc > 0 ? (int)(width - d) : (int)width;
+  const long row_limit = (long)height - dr;
+  const long nrows = std::max<long>(0, std::min<long>((long)row_end, row_limit));
+  p.nrows = (int)nrows;
+  p.ch0 = p.col_begin / 16;
+  p.nch = (p.col_end + 15) / 16 - p.ch0;
+  p.items = (long long)nrows * p.nch;
+  g.empty = p.items == 0 || p.col_end <= p.col_begin;
+  p.step_r = tfg::kThreads / std::max(p.nch, 1);
+  p.step_j = tfg::kThreads % std::max(p.nch, 1);
+  // quantisation mode
+  (void)pixel_levels;
+  return g;
+}
+
+int quant_mode(int pixel_levels, int levels, uint32_t* mask, int* shift) {
+  *mask = 0;
+  *shift = 0;
+  if (levels == 256) return tfg::Q_NONE;
+  if (pixel_levels == levels) {
+    *mask = (uint32_t)(levels - 1) * 0x01010101u;
+    return tfg::Q_CLAMP;
+  }
+  if ((levels & (levels - 1)) == 0) {
+    int lg = 0;
+    while ((1 << lg) < levels) ++lg;
+    *shift = 8 - lg;
+    *mask = (uint32_t)(levels - 1) * 0x01010101u;
+    return tfg::Q_SHIFT;
+  }
+  return tfg::Q_MUL;
+}
+
+// Enqueue the vote of one (d, theta) for n_bands bands into d_glcm (added).
+void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
+                 size_t band_stride, int n_bands, size_t row_end, int pixel_levels, int levels,
+                 int distance, int angle, unsigned flags, unsigned long long* d_glcm, cudaStream_t s) {
+  VoteGeometry g = make_geometry(width, height, pitch, row_end, levels, pixel_levels, distance, angle);
+  if (g.empty) return;
+  tfg::VoteParams& p = g.p;
+  p.img = d_img;
+  p.band_stride = band_stride;
+  p.glcm = d_glcm;
+  const int quant = quant_mode(pixel_levels, levels, &p.qmask, &p.qshift);
+  const size_t cells = (size_t)levels * levels;
+
+  if (flags & TFG_SCHEME_GLOBAL) {
+    VoteKernel fn = pick_global(quant, g.ksel);
+    const long long blocks = std::min<long long>((p.items + 255) / 256, (long long)ctx->num_sms * 16);
+    dim3 grid((unsigned)std::max<long long>(blocks, 1), (unsigned)n_bands);
+    fn<<<grid, 256, 0, s>>>(p);
+    ck(cudaGetLastError(), "glcm_vote_global_kernel launch");
+    ctx->launches++;
+    return;
+  }
+
+  const int strat = pick_strategy(levels, flags);
+  const size_t words = hist_words_of(strat, levels);
+  const size_t smem = words * 4;
+  p.hist_words = (int)words;
+  VoteKernel fn = pick_vote(quant, strat, g.ksel);
+  const int bps = occupancy_for(fn, smem);
+  // persistent-style grid: at most one wave of CTAs per band set, and no CTA
+  // with less than one round of work.
+  long long per_band = std::max<long long>(1, (long long)ctx->num_sms * bps / std::max(n_bands, 1));
+  per_band = std::min<long long>(per_band, (p.items + tfg::kRoundItems - 1) / tfg::kRoundItems);
+  per_band = std::max<long long>(per_band, 1);
+  p.items_per_cta = (p.items + per_band - 1) / per_band;
+  const bool use_partials = cells > 4096;
+  if (use_partials) {
+    const size_t bytes = (size_t)per_band * n_bands * cells * 4;
+    p.partials = static_cast<uint32_t*>(ctx->partials.get(bytes));
+  }
+  dim3 grid((unsigned)per_band, (unsigned)n_bands);
+  fn<<<grid, tfg::kThreads, smem, s>>>(p);
+  ck(cudaGetLastError(), "glcm_vote_kernel launch");
+  ctx->launches++;
+  if (use_partials) {
+    const long long total = (long long)cells * n_bands;
+    const int rblocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx->num_sms * 8);
+    tfg::glcm_reduce_partials_kernel<<<rblocks, 256, 0, s>>>(p.partials, (int)per_band, (int)cells,
+                                                            n_bands, d_glcm);
+    ck(cudaGetLastError(), "glcm_reduce_partials_kernel launch");
+    ctx->launches++;
+  }
+}
+
+void launch_validate(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t rows, size_t pitch,
+                     size_t band_stride, int n_bands, int levels, int* d_err, cudaStream_t s) {
+  if (levels == 256) return;
+  const long long items = (long long)rows * ((width + 15) / 16);
+  const int blocks = (int)std::min<long long>((items + 255) / 256, (long long)ctx->num_sms * 8);
+  dim3 grid(std::max(blocks, 1), n_bands);
+  tfg::validate_levels_kernel<<<grid, 256, 0, s>>>(d_img, pitch, (int)width, (long long)rows, band_stride,
+                                                   levels, d_err);
+  ck(cudaGetLastError(), "validate_levels_kernel launch");
+  ctx->launches++;
+}
+
+size_t round16(size_t v) { return (v + 15) & ~size_t(15); }
+
+void check_dts(const int* distances, const int* angles, int n_dt, size_t width, size_t height) {
+  if (n_dt < 1 || !distances || !angles) fail(TFG_INVALID_ARGUMENT, "glcm: need at least one (distance, angle)");
+  for (int i = 0; i < n_dt; ++i) {
+    check_angle(angles[i]);
+    check_geometry(width, height, distances[i]);
+  }
+}
+
+void check_pixel_levels(int pixel_levels, int levels) {
+  if (pixel_levels != 256 && pixel_levels != levels)
+    fail(TFG_INVALID_ARGUMENT, "glcm: image levels do not match params levels");
+}
+
+// Post-processing of n GLCMs resident at d_counts; results to host buffers.
+void finish(tfg_ctx* ctx, unsigned long long* d_counts, int n, int levels, unsigned flags,
+            uint64_t* counts_out, double* probs_out, double* feats_out, cudaStream_t s) {
+  const size_t cells = (size_t)levels * levels;
+  unsigned long long* d_final = d_counts;
+  if (flags & TFG_SYMMETRIC) {
+    d_final = static_cast<unsigned long long*>(ctx->sym.get(n * cells * 8));
+    dim3 grid((unsigned)std::min<size_t>((cells + 255) / 256, 1024), (unsigned)n);
+    tfg::symmetrize_kernel<<<grid, 256, 0, s>>>(d_counts, levels, d_final);
+    ck(cudaGetLastError(), "symmetrize launch");
+    ctx->launches++;
+  }
+  const bool want_probs = (flags & (TFG_NORMALIZE | TFG_FEATURES)) != 0;
+  int* d_errs = nullptr;
+  double* d_probs = nullptr;
+  double* d_feats = nullptr;
+  if (want_probs) {
+    d_errs = static_cast<int*>(ctx->errs.get(2 * n * sizeof(int)));
+    ck(cudaMemsetAsync(d_errs, 0, 2 * n * sizeof(int), s), "memset");
+    d_probs = static_cast<double*>(ctx->probs.get(n * cells * 8));
+    tfg::normalize_kernel<<<n, 1024, 0, s>>>(d_final, levels, d_probs, d_errs);
+    ck(cudaGetLastError(), "normalize launch");
+    ctx->launches++;
+    if (flags & TFG_FEATURES) {
+      d_feats = static_cast<double*>(ctx->feats.get(n * 5 * 8));
+      tfg::features_kernel<<<n, 1024, 0, s>>>(d_probs, levels, d_feats, d_errs + n);
+      ck(cudaGetLastError(), "features launch");
+      ctx->launches++;
+    }
+  }
+  // stage everything through pinned memory, one sync
+  const size_t b_counts = n * cells * 8, b_probs = want_probs ? n * cells * 8 : 0;
+  const size_t b_feats = d_feats ? n * 5 * 8 : 0, b_err = want_probs ? 2 * n * sizeof(int) : 0;
+  char* h = static_cast<char*>(ctx->hout.get(b_counts + b_probs + b_feats + b_err + 64));
+  ck(cudaMemcpyAsync(h, d_final, b_counts, cudaMemcpyDeviceToHost, s), "D2H counts");
+  if (b_probs) ck(cudaMemcpyAsync(h + b_counts, d_probs, b_probs, cudaMemcpyDeviceToHost, s), "D2H probs");
+  if (b_feats) ck(cudaMemcpyAsync(h + b_counts + b_probs, d_feats, b_feats, cudaMemcpyDeviceToHost, s), "D2H feats");
+  if (b_err) ck(cudaMemcpyAsync(h + b_counts + b_probs + b_feats, d_errs, b_err, cudaMemcpyDeviceToHost, s), "D2H err");
+  ck(cudaStreamSynchronize(s), "stream sync");
+  if (b_err) {
+    const int* e = reinterpret_cast<const int*>(h + b_counts + b_probs + b_feats);
+    for (int i = 0; i < n; ++i)
+      if (e[i]) fail(TFG_INVALID_ARGUMENT, "normalize: all-zero matrix");
+    if (d_feats)
+      for (int i = 0; i < n; ++i)
+        if (e[n + i]) fail(TFG_INVALID_ARGUMENT, "extract_features: input is not normalized");
+  }
+  if (counts_out) std::memcpy(counts_out, h, b_counts);
+  if (probs_out && b_probs) std::memcpy(probs_out, h + b_counts, b_probs);
+  if (feats_out && b_feats) std::memcpy(feats_out, h + b_counts + b_probs, b_feats);
+}
+
+void check_async_flag(tfg_ctx* ctx, cudaStream_t s) {
+  int flag = 0;
+  ck(cudaMemcpyAsync(&flag, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H err");
+  ck(cudaStreamSynchronize(s), "stream sync");
+  if (flag) {
+    ck(cudaMemset(ctx->d_err, 0, sizeof(int)), "memset");
+    fail(TFG_INVALID_ARGUMENT, "QuantizedImage: pixel value exceeds gray level");
+  }
+}
+
+size_t auto_chunks(size_t width, size_t height, int max_d) {
+  const size_t bytes = width * height;
+  const size_t target = 32u << 20;  // ~32 MiB per chunk
+  size_t k = (bytes + target - 1) / target;
+  const size_t cap = height / (size_t)(max_d + 1);
+  if (k > cap) k = cap;
+  return std::max<size_t>(k, 1);
+}
+
+// Chunk specs, partition() semantics (pipeline.hpp:48-73) with the largest
+// halo any requested (d, theta) needs.
+std::vector<uint64_t> chunk_specs(size_t width, size_t height, const int* distances, const int* angles,
+                                  int n_dt, size_t k) {
+  int halo = 0, dmax = 1;
+  for (int i = 0; i < n_dt; ++i) {
+    dmax = std::max(dmax, distances[i]);
+    if (angles[i] != 0) halo = std::max(halo, distances[i]);
+  }
+  if (k < 1 || k > height) fail(TFG_INVALID_ARGUMENT, "partition: chunk count must be in [1, height]");
+  if (height / k <= (size_t)dmax && k > 1)
+    fail(TFG_INVALID_ARGUMENT, "partition: too many chunks for this distance (chunk shorter than halo)");
+  (void)width;
+  std::vector<uint64_t> s(3 * k);
+  const size_t base = height / k, extra = height % k;
+  size_t row = 0;
+  for (size_t i = 0; i < k; ++i) {
+    const size_t end = row + base + (i < extra ? 1 : 0);
+    s[3 * i] = row;
+    s[3 * i + 1] = end;
+    s[3 * i + 2] = i + 1 == k ? end : std::min(height, end + (size_t)halo);
+    row = end;
+  }
+  return s;
+}
+
+// Scheme 3 pipeline over host rows. `fetch_rows(i, start, end, dst_host_or_null)`
+// either fills a pinned slot (returns that pointer) or returns a pointer to
+// the caller's own host rows.
+template <typename Fetch>
+void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, int levels,
+                  const int* distances, const int* angles, int n_dt, size_t k, unsigned flags,
+                  unsigned long long* d_acc, Fetch&& fetch_rows) {
+  const std::vector<uint64_t> specs = chunk_specs(width, height, distances, angles, n_dt, k);
+  const size_t pitch = round16(width);
+  size_t max_rows = 0;
+  for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, specs[3 * i + 2] - specs[3 * i]);
+  const bool sequential = (flags & TFG_SEQUENTIAL) != 0;
+  for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->dslot[sl].get(max_rows * pitch + 64);
+  for (size_t i = 0; i < k; ++i) {
+    const int sl = (int)(i % tfg_ctx::kSlots);
+    const size_t start = specs[3 * i], owned_end = specs[3 * i + 1], buf_end = specs[3 * i + 2];
+    const size_t rows = buf_end - start;
+    // host side: the slot's previous H2D must be done before we refill it
+    if (i >= (size_t)tfg_ctx::kSlots) ck(cudaEventSynchronize(ctx->copied[sl]), "event sync");
+    const uint8_t* src = fetch_rows(i, start, owned_end, buf_end, sl);
+    uint8_t* dst = static_cast<uint8_t*>(ctx->dslot[sl].p);
+    // device side: the slot's previous votes must be done before overwrite
+    if (i >= (size_t)tfg_ctx::kSlots) ck(cudaStreamWaitEvent(ctx->copy, ctx->consumed[sl], 0), "wait");
+    ck(cudaMemcpy2DAsync(dst, pitch, src, width, width, rows, cudaMemcpyHostToDevice, ctx->copy), "H2D chunk");
+    ck(cudaEventRecord(ctx->copied[sl], ctx->copy), "event record");
+    ck(cudaStreamWaitEvent(ctx->exec, ctx->copied[sl], 0), "wait");
+    if (pixel_levels == levels) launch_validate(ctx, dst, width, rows, pitch, 0, 1, levels, ctx->d_err, ctx->exec);
+    for (int t = 0; t < n_dt; ++t)
+      launch_vote(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, levels, distances[t],
+                  angles[t], flags, d_acc + (size_t)t * levels * levels, ctx->exec);
+    ck(cudaEventRecord(ctx->consumed[sl], ctx->exec), "event record");
+    if (sequential) ck(cudaStreamSynchronize(ctx->exec), "stream sync");
+  }
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int tfg_abi_version(void) { return TFG_ABI_VERSION; }
+const char* tfg_last_error(void) { return g_error.c_str(); }
+size_t tfg_last_error_chunk(void) { return g_error_chunk; }
+uint64_t tfg_launch_count(tfg_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+int tfg_ctx_create(tfg_ctx** out, int device, unsigned flags) {
+  (void)flags;
+  if (!out) {
+    g_error = "tfg_ctx_create: null output";
+    return TFG_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  tfg_ctx* ctx = new tfg_ctx();
+  const int rc = guarded([&] {
+    int n = 0;
+    ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) fail(TFG_INVALID_ARGUMENT, "tfg_ctx_create: no such CUDA device");
+    ctx->device = device;
+    DeviceGuard dg(device);
+    ck(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    ck(cudaStreamCreateWithFlags(&ctx->exec, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "stream");
+    for (int i = 0; i < tfg_ctx::kSlots; ++i) {
+      ck(cudaEventCreateWithFlags(&ctx->copied[i], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&ctx->consumed[i], cudaEventDisableTiming), "event");
+    }
+    ck(cudaMalloc(&ctx->d_err, 64), "cudaMalloc");
+    ck(cudaMemset(ctx->d_err, 0, 64), "memset");
+  });
+  if (rc != TFG_OK) {
+    tfg_ctx_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return TFG_OK;
+}
+
+void tfg_ctx_destroy(tfg_ctx* ctx) {
+  if (!ctx) return;
+  {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    if (ctx->exec) cudaStreamSynchronize(ctx->exec);
+    if (ctx->copy) cudaStreamSynchronize(ctx->copy);
+    for (auto& b : ctx->dslot) b.release();
+    for (auto& b : ctx->hslot) b.release();
+    ctx->img.release();
+    ctx->acc.release();
+    ctx->sym.release();
+    ctx->probs.release();
+    ctx->feats.release();
+    ctx->partials.release();
+    ctx->qbuf.release();
+    ctx->tmp.release();
+    ctx->errs.release();
+    ctx->hout.release();
+    for (int i = 0; i < tfg_ctx::kSlots; ++i) {
+      if (ctx->copied[i]) cudaEventDestroy(ctx->copied[i]);
+      if (ctx->consumed[i]) cudaEventDestroy(ctx->consumed[i]);
+    }
+    if (ctx->d_err) cudaFree(ctx->d_err);
+    if (ctx->exec) cudaStreamDestroy(ctx->exec);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  delete ctx;
+}
+
+int tfg_neighbor_offset(int distance, int angle_deg, long* drow, long* dcol) {
+  return guarded([&] {
+    if (!offset_of(distance, angle_deg, drow, dcol)) fail(TFG_INVALID_ARGUMENT, "neighbor_offset: bad angle");
+  });
+}
+
+int tfg_valid_pair_count(size_t width, size_t height, int distance, int angle_deg, uint64_t* out) {
+  return guarded([&] {
+    const size_t d = (size_t)distance;
+    if (distance < 1 || d >= width || d >= height)
+      fail(TFG_INVALID_ARGUMENT,
+           "valid_pair_count: degenerate geometry (d must be in [1, min(width, height)))");
+    switch (angle_deg) {
+      case 0: *out = (uint64_t)height * (width - d); break;
+      case 90: *out = (uint64_t)(height - d) * width; break;
+      case 45:
+      case 135: *out = (uint64_t)(height - d) * (width - d); break;
+      default: fail(TFG_INVALID_ARGUMENT, "valid_pair_count: bad angle");
+    }
+  });
+}
+
+int tfg_partition(size_t width, size_t height, int distance, int angle_deg, size_t chunk_count,
+                  uint64_t* specs_out) {
+  return guarded([&] {
+    const size_t d = (size_t)distance;
+    if (distance < 1 || d >= width || d >= height)
+      fail(TFG_INVALID_ARGUMENT, "partition: degenerate geometry (d must be in [1, min(width, height)))");
+    check_angle(angle_deg);
+    if (chunk_count < 1 || chunk_count > height)
+      fail(TFG_INVALID_ARGUMENT, "partition: chunk count must be in [1, height]");
+    if (height / chunk_count <= d && chunk_count > 1)
+      fail(TFG_INVALID_ARGUMENT, "partition: too many chunks for this distance (chunk shorter than halo)");
+    auto s = chunk_specs(width, height, &distance, &angle_deg, 1, chunk_count);
+    std::memcpy(specs_out, s.data(), s.size() * 8);
+  });
+}
+
+int tfg_plan(int levels, size_t scratch_budget, unsigned worker_count, unsigned* copies,
+             unsigned* groups_per_unit, int* degraded) {
+  return guarded([&] {
+    check_levels(levels, "plan");
+    (void)worker_count;
+    const size_t sub = (size_t)levels * levels * 4;  // u32 sub-GLCM (parallel.hpp:48)
+    size_t c = scratch_budget / (2 * sub);
+    if (c >= 1) {
+      *groups_per_unit = 2;
+      *degraded = 0;
+    } else {
+      *groups_per_unit = 1;
+      *degraded = 1;
+      c = scratch_budget / sub;
+      if (c < 1) c = 1;
+    }
+    *copies = (unsigned)std::min<size_t>(c, 8);
+  });
+}
+
+int tfg_quantize(tfg_ctx* ctx, const uint8_t* gray, size_t n, int levels, uint8_t* out, unsigned flags) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded([&] {
+    check_levels(levels, "quantize");
+    if (n == 0) return;
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = ctx->exec;
+    const size_t n16 = round16(n);
+    const uint8_t* d_in = gray;
+    uint8_t* d_out = out;
+    uint8_t* buf = nullptr;
+    const bool dev = (flags & TFG_INPUT_DEVICE) != 0;
+    if (!dev) {
+      buf = static_cast<uint8_t*>(ctx->qbuf.get(2 * n16));
+      ck(cudaMemcpyAsync(buf, gray, n, cudaMemcpyHostToDevice, s), "H2D");
+      d_in = buf;
+      d_out = buf + n16;
+    } else if ((reinterpret_cast<uintptr_t>(gray) | reinterpret_cast<uintptr_t>(out)) & 15) {
+      fail(TFG_INVALID_ARGUMENT, "quantize: device buffers must be 16-byte aligned");
+    }
+    const int blocks = (int)std::min<size_t>((n / 16 + 255) / 256 + 1, (size_t)ctx->num_sms * 8);
+    tfg::quantize_kernel<<<blocks, 256, 0, s>>>(d_in, d_out, (long long)n, levels);
+    ck(cudaGetLastError(), "quantize launch");
+    ctx->launches++;
+    if (!dev) ck(cudaMemcpyAsync(out, d_out, n, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t pitch,
+                   size_t band_stride, size_t n_bands, int pixel_levels, int levels, const int* distances,
+                   const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out, double* probs_out,
+                   double* feats_out) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded([&] {
+    check_levels(levels, "glcm");
+    check_pixel_levels(pixel_levels, levels);
+    if (width == 0 || height == 0) fail(TFG_INVALID_ARGUMENT, "QuantizedImage: dimensions must be positive");
+    if (pitch < width) fail(TFG_INVALID_ARGUMENT, "glcm: pitch must be >= width");
+    if (n_bands < 1) fail(TFG_INVALID_ARGUMENT, "glcm: need at least one band");
+    if (n_bands > 1 && band_stride < pitch * height) fail(TFG_INVALID_ARGUMENT, "glcm: bands overlap");
+    check_dts(distances, angles_deg, n_dt, width, height);
+    if (!px) fail(TFG_INVALID_ARGUMENT, "glcm: null pixels");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = ctx->exec;
+    const size_t cells = (size_t)levels * levels;
+    const size_t n_out = n_bands * (size_t)n_dt;
+    auto* d_acc = static_cast<unsigned long long*>(ctx->acc.get(n_out * cells * 8));
+    ck(cudaMemsetAsync(d_acc, 0, n_out * cells * 8, s), "memset");
+    const bool dev = (flags & TFG_INPUT_DEVICE) != 0;
+
+    if (!dev && n_bands == 1) {
+      // host image -> Scheme-3 stream pipeline (copy chunk i+1 while voting chunk i)
+      int dmax = 1;
+      for (int i = 0; i < n_dt; ++i) dmax = std::max(dmax, distances[i]);
+      const size_t k = auto_chunks(width, height, dmax);
+      // per-(d,theta) accumulators are contiguous: d_acc + t*cells
+      run_pipeline(ctx, width, height, pixel_levels, levels, distances, angles_deg, n_dt, k, flags, d_acc,
+                   [&](size_t, size_t start, size_t, size_t, int) -> const uint8_t* {
+                     if (pitch != width) fail(TFG_INVALID_ARGUMENT, "glcm: host images must be dense (pitch == width)");
+                     return px + start * width;
+                   });
+      if (pixel_levels == levels) check_async_flag(ctx, s);
+      finish(ctx, d_acc, (int)n_out, levels, flags, counts_out, probs_out, feats_out, s);
+      return;
+    }
+
+    const uint8_t* d_img = px;
+    size_t dpitch = pitch, dstride = band_stride;
+    const bool aligned = dev && ((reinterpret_cast<uintptr_t>(px) & 15) == 0) && (pitch % 16 == 0) &&
+                         (n_bands == 1 || band_stride % 16 == 0);
+    if (!aligned) {
+      // stage into an aligned, pitched device buffer (one copy per band)
+      dpitch = round16(width);
+      dstride = dpitch * height;
+      uint8_t* buf = static_cast<uint8_t*>(ctx->img.get(dstride * n_bands + 64));
+      for (size_t b = 0; b < n_bands; ++b)
+        ck(cudaMemcpy2DAsync(buf + b * dstride, dpitch, px + b * band_stride, pitch, width, height,
+                             dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s),
+           "stage image");
+      d_img = buf;
+    }
+    if (pixel_levels == levels)
+      launch_validate(ctx, d_img, width, height, dpitch, dstride, (int)n_bands, levels, ctx->d_err, s);
+    for (int t = 0; t < n_dt; ++t) {
+      // bands are batched in one launch (blockIdx.y = band); outputs band-major
+      // [band][dt][cell]: launch per dt writing with a band stride of n_dt*cells.
+      if (n_dt == 1) {
+        launch_vote(ctx, d_img, width, height, dpitch, dstride, (int)n_bands, height, pixel_levels, levels,
+                    distances[t], angles_deg[t], flags, d_acc, s);
+      } else {
+        // per-dt scratch then scatter into band-major layout
+        auto* tmp = static_cast<unsigned long long*>(ctx->tmp.get(n_bands * cells * 8));
+        ck(cudaMemsetAsync(tmp, 0, n_bands * cells * 8, s), "memset");
+        launch_vote(ctx, d_img, width, height, dpitch, dstride, (int)n_bands, height, pixel_levels, levels,
+                    distances[t], angles_deg[t], flags, tmp, s);
+        ck(cudaMemcpy2DAsync(d_acc + (size_t)t * cells, (size_t)n_dt * cells * 8, tmp, cells * 8, cells * 8,
+                             n_bands, cudaMemcpyDeviceToDevice, s),
+           "scatter");
+      }
+    }
+    if (pixel_levels == levels) check_async_flag(ctx, s);
+    finish(ctx, d_acc, (int)n_out, levels, flags, counts_out, probs_out, feats_out, s);
+  });
+}
+
+int tfg_glcm(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t pitch, int pixel_levels,
+             int levels, const int* distances, const int* angles_deg, int n_dt, unsigned flags,
+             uint64_t* counts_out, double* probs_out, double* feats_out) {
+  return tfg_glcm_bands(ctx, px, width, height, pitch, pitch * height, 1, pixel_levels, levels, distances,
+                        angles_deg, n_dt, flags, counts_out, probs_out, feats_out);
+}
+
+int tfg_glcm_chunked(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, int levels,
+                     const int* distances, const int* angles_deg, int n_dt, size_t chunk_count,
+                     tfg_fetch_fn fetch, void* user, unsigned flags, uint64_t* counts_out, double* probs_out,
+                     double* feats_out) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded([&] {
+    check_levels(levels, "glcm");
+    check_pixel_levels(pixel_levels, levels);
+    if (!fetch) fail(TFG_INVALID_ARGUMENT, "glcm_chunked: null fetch callback");
+    check_dts(distances, angles_deg, n_dt, width, height);
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = ctx->exec;
+    const size_t cells = (size_t)levels * levels;
+    auto* d_acc = static_cast<unsigned long long*>(ctx->acc.get((size_t)n_dt * cells * 8));
+    ck(cudaMemsetAsync(d_acc, 0, (size_t)n_dt * cells * 8, s), "memset");
+    const std::vector<uint64_t> specs = chunk_specs(width, height, distances, angles_deg, n_dt, chunk_count);
+    size_t max_rows = 0;
+    for (size_t i = 0; i < chunk_count; ++i) max_rows = std::max<size_t>(max_rows, specs[3 * i + 2] - specs[3 * i]);
+    for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->hslot[sl].get(max_rows * width + 64);
+    try {
+      run_pipeline(ctx, width, height, pixel_levels, levels, distances, angles_deg, n_dt, chunk_count, flags, d_acc,
+                   [&](size_t i, size_t start, size_t owned_end, size_t buf_end, int sl) -> const uint8_t* {
+                     uint8_t* dst = static_cast<uint8_t*>(ctx->hslot[sl].p);
+                     char msg[512] = {0};
+                     const int rc = fetch(user, i, start, owned_end, buf_end, dst, msg, sizeof msg);
+                     if (rc) {
+                       g_error_chunk = i;
+                       fail(TFG_SOURCE_ERROR, "chunk " + std::to_string(i) + ": " +
+                                                  (msg[0] ? std::string(msg) : std::string("source failure")));
+                     }
+                     return dst;
+                   });
+    } catch (...) {
+      cudaStreamSynchronize(ctx->exec);
+      cudaStreamSynchronize(ctx->copy);
+      throw;
+    }
+    if (pixel_levels == levels) check_async_flag(ctx, s);
+    finish(ctx, d_acc, n_dt, levels, flags, counts_out, probs_out, feats_out, s);
+  });
+}
+
+int tfg_symmetrize(tfg_ctx* ctx, const uint64_t* counts, int levels, uint64_t* out) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded([&] {
+    check_levels(levels, "Glcm");
+    DeviceGuard dg(ctx->device);
+    const size_t cells = (size_t)levels * levels;
+    auto* d = static_cast<unsigned long long*>(ctx->acc.get(cells * 8));
+    ck(cudaMemcpyAsync(d, counts, cells * 8, cudaMemcpyHostToDevice, ctx->exec), "H2D");
+    finish(ctx, d, 1, levels, TFG_SYMMETRIC, out, nullptr, nullptr, ctx->exec);
+  });
+}
+
+int tfg_normalize(tfg_ctx* ctx, const uint64_t* counts, int levels, double* out) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded([&] {
+    check_levels(levels, "Glcm");
+    DeviceGuard dg(ctx->device);
+    const size_t cells = (size_t)levels * levels;
+    auto* d = static_cast<unsigned long long*>(ctx->acc.get(cells * 8));
+    ck(cudaMemcpyAsync(d, counts, cells * 8, cudaMemcpyHostToDevice, ctx->exec), "H2D");
+    finish(ctx, d, 1, levels, TFG_NORMALIZE, nullptr, out, nullptr, ctx->exec);
+  });
+}
+
+int tfg_features(tfg_ctx* ctx, const double* probs, int levels, double* out5) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded([&] {
+    if (levels < 1 || levels > 256) fail(TFG_INVALID_ARGUMENT, "extract_features: levels must be in [1, 256]");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = ctx->exec;
+    const size_t cells = (size_t)levels * levels;
+    auto* d_p = static_cast<double*>(ctx->probs.get(cells * 8));
+    auto* d_f = static_cast<double*>(ctx->feats.get(5 * 8));
+    int* d_e = static_cast<int*>(ctx->errs.get(2 * sizeof(int)));
+    ck(cudaMemcpyAsync(d_p, probs, cells * 8, cudaMemcpyHostToDevice, s), "H2D");
+    ck(cudaMemsetAsync(d_e, 0, 2 * sizeof(int), s), "memset");
+    tfg::features_kernel<<<1, 1024, 0, s>>>(d_p, levels, d_f, d_e);
+    ck(cudaGetLastError(), "features launch");
+    ctx->launches++;
+    int e = 0;
+    double* h = static_cast<double*>(ctx->hout.get(64));
+    ck(cudaMemcpyAsync(h, d_f, 5 * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaMemcpyAsync(&e, d_e, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+    if (e) fail(TFG_INVALID_ARGUMENT, "extract_features: input is not normalized");
+    std::memcpy(out5, h, 5 * 8);
+  });
+}
+
+int tfg_glcm_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t height, size_t pitch, size_t row_end,
+                   int pixel_levels, int levels, int distance, int angle_deg, unsigned flags, uint64_t* d_counts,
+                   void* stream) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  return guarded([&] {
+    check_levels(levels, "glcm");
+    check_pixel_levels(pixel_levels, levels);
+    check_angle(angle_deg);
+    if (distance < 1 || (size_t)distance >= width)
+      fail(TFG_INVALID_ARGUMENT, "glcm: degenerate geometry (d must be in [1, min(width, height)))");
+    if ((reinterpret_cast<uintptr_t>(d_px) & 15) || (pitch % 16) || pitch < width)
+      fail(TFG_INVALID_ARGUMENT, "glcm_async: device image must be 16-byte aligned with pitch % 16 == 0");
+    if (row_end > height) fail(TFG_INVALID_ARGUMENT, "glcm_async: row_end > height");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->exec;
+    if (pixel_levels == levels) launch_validate(ctx, d_px, width, height, pitch, 0, 1, levels, ctx->d_err, s);
+    launch_vote(ctx, d_px, width, height, pitch, 0, 1, row_end, pixel_levels, levels, distance, angle_deg, flags,
+                reinterpret_cast<unsigned long long*>(d_counts), s);
+  });
+}
+
+int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned flags, uint64_t* d_sym_out,
+                   double* d_probs_out, double* d_feats_out, void* stream) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  return guarded([&] {
+    check_levels(levels, "Glcm");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->exec;
+    const size_t cells = (size_t)levels * levels;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(d_counts);
+    if ((flags & TFG_SYMMETRIC) && d_sym_out) {
+      dim3 grid((unsigned)std::min<size_t>((cells + 255) / 256, 1024), 1);
+      tfg::symmetrize_kernel<<<grid, 256, 0, s>>>(src, levels, reinterpret_cast<unsigned long long*>(d_sym_out));
+      ck(cudaGetLastError(), "symmetrize launch");
+      ctx->launches++;
+      src = reinterpret_cast<const unsigned long long*>(d_sym_out);
+    }
+    if ((flags & (TFG_NORMALIZE | TFG_FEATURES)) && d_probs_out) {
+      tfg::normalize_kernel<<<1, 1024, 0, s>>>(src, levels, d_probs_out, ctx->d_err + 1);
+      ck(cudaGetLastError(), "normalize launch");
+      ctx->launches++;
+      if ((flags & TFG_FEATURES) && d_feats_out) {
+        tfg::features_kernel<<<1, 1024, 0, s>>>(d_probs_out, levels, d_feats_out, ctx->d_err + 2);
+        ck(cudaGetLastError(), "features launch");
+        ctx->launches++;
+      }
+    }
+  });
+}
+
+int tfg_check_async_errors(tfg_ctx* ctx) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  return guarded([&] {
+    DeviceGuard dg(ctx->device);
+    ck(cudaDeviceSynchronize(), "sync");
+    int e[3] = {0, 0, 0};
+    ck(cudaMemcpy(e, ctx->d_err, sizeof e, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemset(ctx->d_err, 0, sizeof e), "memset");
+    if (e[0]) fail(TFG_INVALID_ARGUMENT, "QuantizedImage: pixel value exceeds gray level");
+    if (e[1]) fail(TFG_INVALID_ARGUMENT, "normalize: all-zero matrix");
+    if (e[2]) fail(TFG_INVALID_ARGUMENT, "extract_features: input is not normalized");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,546 @@
+"""Python mirror of the reference's ``texforge`` API, backed by the B200 engine.
+
+Names, argument meaning and error behaviour follow the reference's C++ headers
+(R/ = /root/reference/proj/include/texforge/): ``std::invalid_argument``
+becomes ``ValueError`` with the same message text, ``PipelineError`` keeps its
+``chunk_index``.  Every GLCM-producing call runs on the GPU through
+libtexforge_cuda.so (include/texforge_cuda.h); there is no CPU fallback.
+
+Small host-side pieces that the reference also keeps on the host and that are
+O(L^2) or O(K) (ContentionStats from a finished GLCM, merge of per-chunk
+matrices, the row partition arithmetic) are computed here or in the C library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib as L
+
+kDefaultScratchBudget = 49152  # parallel.hpp:16
+
+
+# --------------------------------------------------------------------------- types
+class Angle(enum.IntEnum):
+    """glcm.hpp:15"""
+    deg0 = 0
+    deg45 = 45
+    deg90 = 90
+    deg135 = 135
+
+
+def angle_from_degrees(deg: int) -> Angle:
+    """glcm.hpp:17-25"""
+    try:
+        return Angle(int(deg))
+    except ValueError:
+        raise ValueError("angle must be one of 0, 45, 90, 135") from None
+
+
+def to_degrees(a: Angle) -> int:
+    return int(a)
+
+
+@dataclass
+class GlcmParams:
+    """glcm.hpp:29-33"""
+    distance: int = 1
+    angle: Angle = Angle.deg0
+    levels: int = 8
+
+
+@dataclass(eq=False)
+class GrayImage:
+    """image.hpp:13-28 — 8-bit row-major raster."""
+    width: int
+    height: int
+    pixels: np.ndarray
+
+    def __post_init__(self):
+        self.pixels = np.ascontiguousarray(np.asarray(self.pixels, dtype=np.uint8).reshape(-1))
+        if self.width == 0 or self.height == 0:
+            raise ValueError("GrayImage: dimensions must be positive")
+        if self.pixels.size != self.width * self.height:
+            raise ValueError("GrayImage: pixel count does not match dimensions")
+
+    def at(self, row: int, col: int) -> int:
+        return int(self.pixels[row * self.width + col])
+
+
+@dataclass(eq=False)
+class QuantizedImage:
+    """image.hpp:31-52 — gray levels in [0, levels)."""
+    width: int
+    height: int
+    levels: int
+    pixels: np.ndarray
+
+    def __post_init__(self):
+        self.pixels = np.ascontiguousarray(np.asarray(self.pixels, dtype=np.uint8).reshape(-1))
+        if self.width == 0 or self.height == 0:
+            raise ValueError("QuantizedImage: dimensions must be positive")
+        if self.levels < 2 or self.levels > 256:
+            raise ValueError("QuantizedImage: levels must be in [2, 256]")
+        if self.pixels.size != self.width * self.height:
+            raise ValueError("QuantizedImage: pixel count does not match dimensions")
+        if self.levels < 256 and self.pixels.size and int(self.pixels.max()) >= self.levels:
+            raise ValueError("QuantizedImage: pixel value exceeds gray level")
+
+    def at(self, row: int, col: int) -> int:
+        return int(self.pixels[row * self.width + col])
+
+
+class Glcm:
+    """glcm.hpp:37-60 — L x L u64 counts, row = reference gray, col = anchor gray."""
+
+    def __init__(self, levels: int, counts=None):
+        if levels < 2 or levels > 256:
+            raise ValueError("Glcm: levels must be in [2, 256]")
+        self.levels = int(levels)
+        if counts is None:
+            self.counts = np.zeros(levels * levels, dtype=np.uint64)
+        else:
+            c = np.asarray(counts, dtype=np.uint64).reshape(-1).copy()
+            if c.size != levels * levels:
+                raise ValueError("Glcm: counts length must be levels^2")
+            self.counts = c
+
+    def at(self, row: int, col: int) -> int:
+        return int(self.counts[row * self.levels + col])
+
+    def set(self, row: int, col: int, v: int) -> None:
+        self.counts[row * self.levels + col] = v
+
+    def total(self) -> int:
+        return int(self.counts.sum(dtype=np.uint64))
+
+    def matrix(self) -> np.ndarray:
+        return self.counts.reshape(self.levels, self.levels)
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, Glcm) and self.levels == other.levels
+                and np.array_equal(self.counts, other.counts))
+
+    def __repr__(self) -> str:
+        return f"Glcm(levels={self.levels}, total={self.total()})"
+
+
+@dataclass
+class GlcmProbabilities:
+    """glcm.hpp:159-164"""
+    levels: int
+    values: np.ndarray
+
+    def at(self, row: int, col: int) -> float:
+        return float(self.values[row * self.levels + col])
+
+
+@dataclass
+class FeatureVector:
+    """features.hpp:11-17"""
+    energy: float = 0.0
+    contrast: float = 0.0
+    homogeneity: float = 0.0
+    entropy: float = 0.0
+    correlation: float = 0.0
+
+    def as_array(self) -> np.ndarray:
+        return np.array([self.energy, self.contrast, self.homogeneity, self.entropy, self.correlation])
+
+
+@dataclass
+class PixelOffset:
+    row: int = 0
+    col: int = 0
+
+
+@dataclass
+class ExecutionPlan:
+    """parallel.hpp:20-27 (host-side Eq. 4-6 plan, kept unchanged)."""
+    worker_count: int = 1
+    group_size: int = 512
+    copies: int = 1
+    scratch_budget: int = kDefaultScratchBudget
+    groups_per_unit: int = 2
+    degraded: bool = False
+
+
+@dataclass
+class ContentionStats:
+    """parallel.hpp:29-35"""
+    total_votes: int = 0
+    hottest_cell_votes: int = 0
+    hottest_cell_index: Tuple[int, int] = (0, 0)
+    per_copy_hottest: List[int] = field(default_factory=list)
+    concentration: float = 0.0
+
+
+@dataclass
+class ChunkSpec:
+    """pipeline.hpp:33-43"""
+    index: int = 0
+    owned_row_start: int = 0
+    owned_row_end: int = 0
+    buffer_row_end: int = 0
+    chunk_count: int = 1
+
+    def owned_rows(self) -> int:
+        return self.owned_row_end - self.owned_row_start
+
+    def buffer_rows(self) -> int:
+        return self.buffer_row_end - self.owned_row_start
+
+
+class PipelineError(RuntimeError):
+    """pipeline.hpp:25-29"""
+
+    def __init__(self, index: int, what: str):
+        super().__init__(what if what.startswith(f"chunk {index}:") else f"chunk {index}: {what}")
+        self.chunk_index = index
+
+
+class ChunkExecution(enum.Enum):
+    """pipeline.hpp:205-208"""
+    pipelined = 0
+    sequential = 1
+
+
+class ChunkSource:
+    """pipeline.hpp:77-84 — fetch(spec, out) fills `out` (a uint8 array of
+    exactly buffer_rows()*width bytes, pinned host memory) with the quantised
+    rows [owned_row_start, buffer_row_end)."""
+
+    def width(self) -> int: raise NotImplementedError
+    def height(self) -> int: raise NotImplementedError
+    def levels(self) -> int: raise NotImplementedError
+    def fetch(self, spec: ChunkSpec, out: np.ndarray) -> None: raise NotImplementedError
+
+
+class MemoryChunkSource(ChunkSource):
+    """pipeline.hpp:86-101"""
+
+    def __init__(self, img: QuantizedImage):
+        self._img = img
+
+    def width(self): return self._img.width
+    def height(self): return self._img.height
+    def levels(self): return self._img.levels
+
+    def fetch(self, spec: ChunkSpec, out: np.ndarray) -> None:
+        b = spec.owned_row_start * self._img.width
+        e = spec.buffer_row_end * self._img.width
+        out[:] = self._img.pixels[b:e]
+
+
+# --------------------------------------------------------------------------- engine
+def _ptr(a: np.ndarray, t=C.c_uint8):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+class Engine:
+    """One CUDA context of the engine (device buffers, streams, pinned ring)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = L.load()
+        h = C.c_void_p()
+        L.check(self._lib.tfg_ctx_create(C.byref(h), int(device), 0))
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            self._lib.tfg_ctx_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(self._lib.tfg_launch_count(self.handle))
+
+    # -- raw, multi-(d, theta) entry point -------------------------------------
+    def glcm(self, pixels: np.ndarray, width: int, height: int, levels: int, dts: Sequence[Tuple[int, int]],
+             pixel_levels: int = 256, flags: int = 0, n_bands: int = 1,
+             want_probs: bool = False, want_features: bool = False):
+        """counts[n_bands, n_dt, L, L] (+ probs, features) of host pixels."""
+        px = np.ascontiguousarray(pixels, dtype=np.uint8).reshape(-1)
+        if px.size != width * height * n_bands:
+            raise ValueError("glcm: pixel count does not match dimensions")
+        n_dt = len(dts)
+        d = (C.c_int * n_dt)(*[int(x[0]) for x in dts])
+        a = (C.c_int * n_dt)(*[int(x[1]) for x in dts])
+        cells = levels * levels
+        counts = np.zeros(n_bands * n_dt * cells, dtype=np.uint64)
+        probs = np.zeros(n_bands * n_dt * cells, dtype=np.float64) if (want_probs or want_features) else None
+        feats = np.zeros(n_bands * n_dt * 5, dtype=np.float64) if want_features else None
+        if want_probs or want_features:
+            flags |= L.TFG_NORMALIZE
+        if want_features:
+            flags |= L.TFG_FEATURES
+        rc = self._lib.tfg_glcm_bands(
+            self.handle, px.ctypes.data_as(C.c_void_p), width, height, width, width * height, n_bands,
+            pixel_levels, levels, d, a, n_dt, flags, _ptr(counts, C.c_uint64),
+            _ptr(probs, C.c_double) if probs is not None else None,
+            _ptr(feats, C.c_double) if feats is not None else None)
+        L.check(rc)
+        counts = counts.reshape(n_bands, n_dt, levels, levels)
+        out = [counts]
+        if want_probs:
+            out.append(probs.reshape(n_bands, n_dt, levels, levels))
+        if want_features:
+            out.append(feats.reshape(n_bands, n_dt, 5))
+        return out[0] if len(out) == 1 else tuple(out)
+
+    def chunked(self, source: ChunkSource, dts: Sequence[Tuple[int, int]], chunk_count: int,
+                pixel_levels: int, levels: int, flags: int = 0) -> np.ndarray:
+        width, height = source.width(), source.height()
+        n_dt = len(dts)
+        d = (C.c_int * n_dt)(*[int(x[0]) for x in dts])
+        a = (C.c_int * n_dt)(*[int(x[1]) for x in dts])
+        counts = np.zeros(n_dt * levels * levels, dtype=np.uint64)
+        err_box = {}
+
+        def _fetch(user, idx, start, owned_end, buf_end, dst, err, err_len):
+            try:
+                spec = ChunkSpec(int(idx), int(start), int(owned_end), int(buf_end), int(chunk_count))
+                out = np.ctypeslib.as_array(dst, shape=(int(buf_end - start) * width,))
+                source.fetch(spec, out)
+                return 0
+            except BaseException as e:  # noqa: BLE001 — any source failure aborts the pipeline
+                err_box["exc"] = e
+                msg = str(e).encode()[: max(0, err_len - 1)]
+                C.memmove(err, msg, len(msg))
+                return 1
+
+        cb = L.FETCH_FN(_fetch)
+        rc = self._lib.tfg_glcm_chunked(self.handle, width, height, pixel_levels, levels, d, a, n_dt,
+                                        int(chunk_count), cb, None, flags, _ptr(counts, C.c_uint64), None, None)
+        if rc == L.TFG_SOURCE_ERROR:
+            idx = int(self._lib.tfg_last_error_chunk())
+            exc = err_box.get("exc")
+            if isinstance(exc, PipelineError):
+                raise exc
+            raise PipelineError(idx, self._lib.tfg_last_error().decode(errors="replace"))
+        L.check(rc)
+        return counts.reshape(n_dt, levels, levels)
+
+    def quantize(self, gray: np.ndarray, levels: int) -> np.ndarray:
+        g = np.ascontiguousarray(gray, dtype=np.uint8).reshape(-1)
+        out = np.empty_like(g)
+        L.check(self._lib.tfg_quantize(self.handle, g.ctypes.data_as(C.c_void_p), g.size, int(levels),
+                                       out.ctypes.data_as(C.c_void_p), 0))
+        return out
+
+    def symmetrize(self, counts: np.ndarray, levels: int) -> np.ndarray:
+        c = np.ascontiguousarray(counts, dtype=np.uint64).reshape(-1)
+        out = np.empty_like(c)
+        L.check(self._lib.tfg_symmetrize(self.handle, _ptr(c, C.c_uint64), int(levels), _ptr(out, C.c_uint64)))
+        return out
+
+    def normalize(self, counts: np.ndarray, levels: int) -> np.ndarray:
+        c = np.ascontiguousarray(counts, dtype=np.uint64).reshape(-1)
+        out = np.empty(c.size, dtype=np.float64)
+        L.check(self._lib.tfg_normalize(self.handle, _ptr(c, C.c_uint64), int(levels), _ptr(out, C.c_double)))
+        return out
+
+    def features(self, probs: np.ndarray, levels: int) -> np.ndarray:
+        p = np.ascontiguousarray(probs, dtype=np.float64).reshape(-1)
+        out = np.empty(5, dtype=np.float64)
+        L.check(self._lib.tfg_features(self.handle, _ptr(p, C.c_double), int(levels), _ptr(out, C.c_double)))
+        return out
+
+
+_engine: Optional[Engine] = None
+_engine_lock = threading.Lock()
+
+
+def default_engine() -> Engine:
+    global _engine
+    with _engine_lock:
+        if _engine is None:
+            _engine = Engine(0)
+        return _engine
+
+
+# --------------------------------------------------------------------------- geometry
+def neighbor_offset(p: GlcmParams) -> PixelOffset:
+    """glcm.hpp:71-80"""
+    dr, dc = C.c_long(), C.c_long()
+    L.check(L.load().tfg_neighbor_offset(int(p.distance), int(p.angle), C.byref(dr), C.byref(dc)))
+    return PixelOffset(dr.value, dc.value)
+
+
+def valid_pair_count(width: int, height: int, p: GlcmParams) -> int:
+    """glcm.hpp:83-94"""
+    out = C.c_uint64()
+    L.check(L.load().tfg_valid_pair_count(int(width), int(height), int(p.distance), int(p.angle), C.byref(out)))
+    return int(out.value)
+
+
+def plan(levels: int, scratch_budget: int = kDefaultScratchBudget, worker_count: Optional[int] = None
+         ) -> ExecutionPlan:
+    """parallel.hpp:39-66 — unchanged host plan (pinned by the reference tests)."""
+    import os
+    if worker_count is None:
+        worker_count = os.cpu_count() or 1
+    if worker_count == 0:
+        worker_count = 1
+    cp, gpu, deg = C.c_uint(), C.c_uint(), C.c_int()
+    L.check(L.load().tfg_plan(int(levels), int(scratch_budget), int(worker_count), C.byref(cp), C.byref(gpu),
+                              C.byref(deg)))
+    return ExecutionPlan(worker_count=int(worker_count), group_size=512, copies=int(cp.value),
+                         scratch_budget=int(scratch_budget), groups_per_unit=int(gpu.value), degraded=bool(deg.value))
+
+
+def partition(width: int, height: int, p: GlcmParams, chunk_count: int) -> List[ChunkSpec]:
+    """pipeline.hpp:48-73"""
+    if chunk_count < 1 or chunk_count > height:
+        # same order of checks as the reference: geometry first
+        if p.distance < 1 or p.distance >= width or p.distance >= height:
+            raise ValueError("partition: degenerate geometry (d must be in [1, min(width, height)))")
+        raise ValueError("partition: chunk count must be in [1, height]")
+    specs = np.zeros(3 * int(chunk_count), dtype=np.uint64)
+    L.check(L.load().tfg_partition(int(width), int(height), int(p.distance), int(p.angle), int(chunk_count),
+                                   _ptr(specs, C.c_uint64)))
+    return [ChunkSpec(i, int(specs[3 * i]), int(specs[3 * i + 1]), int(specs[3 * i + 2]), int(chunk_count))
+            for i in range(int(chunk_count))]
+
+
+# --------------------------------------------------------------------------- inputs
+def synth_noise(width: int, height: int, seed: int) -> GrayImage:
+    """image.hpp:109-116 (bit-identical)."""
+    if width < 2 or height < 2:
+        raise ValueError("synth_noise: dimensions must be >= 2")
+    out = np.empty(width * height, dtype=np.uint8)
+    L.check(L.load().tfg_synth_noise(width, height, seed & 0xFFFFFFFF, _ptr(out)))
+    return GrayImage(width, height, out)
+
+
+def synth_smooth(width: int, height: int, seed: int, threads: int = 0) -> GrayImage:
+    """image.hpp:76-106 (bit-identical; rows generated in parallel)."""
+    if width < 2 or height < 2:
+        raise ValueError("synth_smooth: dimensions must be >= 2")
+    out = np.empty(width * height, dtype=np.uint8)
+    L.check(L.load().tfg_synth_smooth(width, height, seed & 0xFFFFFFFF, _ptr(out), int(threads)))
+    return GrayImage(width, height, out)
+
+
+def quantize(img: GrayImage, levels: int) -> QuantizedImage:
+    """image.hpp:55-62 — on the device."""
+    if levels < 2 or levels > 256:
+        raise ValueError("quantize: levels must be in [2, 256]")
+    q = default_engine().quantize(img.pixels, levels)
+    return QuantizedImage(img.width, img.height, levels, q)
+
+
+# --------------------------------------------------------------------------- GLCM
+def _check_inputs(img: QuantizedImage, p: GlcmParams) -> None:
+    """glcm.hpp:98-104"""
+    if img.levels != p.levels:
+        raise ValueError("glcm: image levels do not match params levels")
+    if p.distance < 1 or p.distance >= img.width or p.distance >= img.height:
+        raise ValueError("glcm: degenerate geometry (d must be in [1, min(width, height)))")
+
+
+def _device_glcm(img: QuantizedImage, p: GlcmParams, flags: int = 0) -> Glcm:
+    _check_inputs(img, p)
+    counts = default_engine().glcm(img.pixels, img.width, img.height, p.levels,
+                                   [(p.distance, int(p.angle))], pixel_levels=p.levels, flags=flags)
+    return Glcm(p.levels, counts.reshape(-1))
+
+
+def stats_from_counts(g: Glcm) -> ContentionStats:
+    """parallel.hpp:91-102 (host, O(L^2) on the finished matrix)."""
+    c = g.counts
+    best = int(np.argmax(c))  # first maximum = lowest flat index on ties
+    total = g.total()
+    hot = int(c[best])
+    return ContentionStats(total_votes=total, hottest_cell_votes=hot,
+                           hottest_cell_index=(best // g.levels, best % g.levels),
+                           concentration=(hot / total) if total else 0.0)
+
+
+def compute_glcm_serial(img: QuantizedImage, p: GlcmParams) -> Glcm:
+    """glcm.hpp:144-147 — identical counts, computed by the device engine."""
+    return _device_glcm(img, p)
+
+
+def compute_glcm_shared(img: QuantizedImage, p: GlcmParams, plan_: ExecutionPlan) -> Tuple[Glcm, ContentionStats]:
+    """parallel.hpp:143-152 — Scheme 1: one global atomic per pixel pair."""
+    g = _device_glcm(img, p, L.TFG_SCHEME_GLOBAL)
+    return g, stats_from_counts(g)
+
+
+def compute_glcm_privatized(img: QuantizedImage, p: GlcmParams, plan_: ExecutionPlan,
+                            group_count: int = 0) -> Tuple[Glcm, ContentionStats]:
+    """parallel.hpp:240-254 — Scheme 2: privatised shared-memory sub-GLCMs."""
+    if plan_.copies < 1:
+        raise ValueError("privatized: plan.copies must be >= 1")
+    g = _device_glcm(img, p)
+    return g, stats_from_counts(g)
+
+
+def contention_profile(img: QuantizedImage, p: GlcmParams) -> ContentionStats:
+    """parallel.hpp:258-260"""
+    return stats_from_counts(compute_glcm_serial(img, p))
+
+
+def reduce_subglcms(subs: Sequence[Sequence[int]], levels: int) -> Glcm:
+    """parallel.hpp:228-237 — elementwise u64 sum (order-independent)."""
+    out = Glcm(levels)
+    for s in subs:
+        a = np.asarray(s, dtype=np.uint64).reshape(-1)
+        if a.size != levels * levels:
+            raise ValueError("reduce_subglcms: sub-GLCM length mismatch")
+        out.counts += a
+    return out
+
+
+def merge_chunk_glcms(parts: Sequence[Glcm]) -> Glcm:
+    """pipeline.hpp:231-240"""
+    if not parts:
+        raise ValueError("merge_chunk_glcms: no parts")
+    out = Glcm(parts[0].levels)
+    for g in parts:
+        if g.levels != out.levels:
+            raise ValueError("merge_chunk_glcms: level mismatch")
+        out.counts += g.counts
+    return out
+
+
+def compute_glcm_chunked(source: ChunkSource, p: GlcmParams, plan_: ExecutionPlan, chunk_count: int,
+                         mode: ChunkExecution = ChunkExecution.pipelined) -> Glcm:
+    """pipeline.hpp:246-337 — Scheme 3 on CUDA streams (pinned ring, H2D on a
+    copy stream overlapped with voting on the exec stream)."""
+    if source.levels() != p.levels:
+        raise ValueError("glcm: image levels do not match params levels")
+    partition(source.width(), source.height(), p, chunk_count)  # same validation + messages
+    flags = L.TFG_SEQUENTIAL if mode == ChunkExecution.sequential else 0
+    counts = default_engine().chunked(source, [(p.distance, int(p.angle))], chunk_count,
+                                      pixel_levels=p.levels, levels=p.levels, flags=flags)
+    return Glcm(p.levels, counts.reshape(-1))
+
+
+def symmetrize(g: Glcm) -> Glcm:
+    """glcm.hpp:150-156"""
+    return Glcm(g.levels, default_engine().symmetrize(g.counts, g.levels))
+
+
+def normalize(g: Glcm) -> GlcmProbabilities:
+    """glcm.hpp:167-177 (bit-exact)."""
+    return GlcmProbabilities(g.levels, default_engine().normalize(g.counts, g.levels))
+
+
+def extract_features(p: GlcmProbabilities) -> FeatureVector:
+    """features.hpp:37-69"""
+    f = default_engine().features(p.values, p.levels)
+    return FeatureVector(*[float(x) for x in f])

@@ -1,0 +1,269 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle and with golden
+vectors produced by the reference itself. Integer GLCMs: bit-exact.
+normalize(): bit-exact. Haralick features: |diff| <= 1e-10 * max(1, |ref|)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1710_06189_b200 import _lib as L
+from paper_1710_06189_b200 import texforge as tf
+
+pytestmark = pytest.mark.gpu
+ANGLES = (0, 45, 90, 135)
+FEAT_TOL = 1e-10
+
+
+def _strategies_for(levels):
+    s = [L.STRAT_PACKED16]
+    if levels * levels * 4 <= 227 * 1024:
+        s.append(L.STRAT_COPY1)
+    if levels * levels * 32 <= 227 * 1024:
+        s.append(L.STRAT_COPIES8)
+    if levels * levels * 128 <= 227 * 1024:
+        s.append(L.STRAT_COPIES32)
+    return s
+
+
+def test_golden_small_cases_auto(engine, small_cases):
+    for c in small_cases:
+        got = engine.glcm(c["pixels"], c["w"], c["h"], c["L"], [(c["d"], c["theta"])],
+                          pixel_levels=c["pixel_levels"])
+        assert np.array_equal(got.reshape(-1), c["counts"]), c
+
+
+def test_golden_small_cases_every_strategy(engine, small_cases):
+    for c in small_cases[::3]:
+        for s in _strategies_for(c["L"]):
+            got = engine.glcm(c["pixels"], c["w"], c["h"], c["L"], [(c["d"], c["theta"])],
+                              pixel_levels=c["pixel_levels"], flags=L.strategy_flag(s))
+            assert np.array_equal(got.reshape(-1), c["counts"]), (s, c["w"], c["h"], c["L"], c["d"], c["theta"])
+
+
+def test_scheme1_global_atomics_matches(engine, small_cases):
+    for c in small_cases[::5]:
+        got = engine.glcm(c["pixels"], c["w"], c["h"], c["L"], [(c["d"], c["theta"])],
+                          pixel_levels=c["pixel_levels"], flags=L.TFG_SCHEME_GLOBAL)
+        assert np.array_equal(got.reshape(-1), c["counts"])
+
+
+@pytest.mark.parametrize("levels", [2, 5, 8, 16, 32, 64, 101, 128, 181, 256])
+def test_random_shapes_vs_oracle(engine, levels):
+    rng = np.random.default_rng(levels)
+    for trial in range(12):
+        w = int(rng.integers(17, 700))
+        h = int(rng.integers(2, 90))
+        gray = rng.integers(0, 256, size=w * h, dtype=np.uint8)
+        ds = sorted({1, 2, 4, int(rng.integers(1, min(w, h))), min(w, h) - 1})
+        dts = [(d, a) for d in ds for a in ANGLES]
+        got = engine.glcm(gray, w, h, levels, dts)
+        for t, (d, a) in enumerate(dts):
+            want = O.glcm_gray(gray, w, h, levels, d, a)
+            assert np.array_equal(got[0, t].reshape(-1), want), (w, h, levels, d, a)
+
+
+def test_large_distance_every_word_shift(engine):
+    # dcol = 16q + 4k + s for every k, s (template KSEL 0..4 and funnel shift)
+    rng = np.random.default_rng(7)
+    w, h = 333, 61
+    gray = rng.integers(0, 256, size=w * h, dtype=np.uint8)
+    dts = [(d, a) for d in range(1, 60) for a in (0, 45, 135)]
+    got = engine.glcm(gray, w, h, 16, dts)
+    for t, (d, a) in enumerate(dts):
+        assert np.array_equal(got[0, t].reshape(-1), O.glcm_gray(gray, w, h, 16, d, a)), (d, a)
+
+
+@pytest.mark.parametrize("levels", [8, 64, 256])
+def test_constant_image_all_votes_one_cell(engine, levels):
+    # 4096^2 constant: every CTA sees > 2^15 votes on ONE cell (PACKED16 spill path,
+    # the run-length shortcut, and the hot-cell case of every strategy).
+    w = h = 2048
+    v = levels - 1
+    img = np.full(w * h, v, dtype=np.uint8)
+    for s in _strategies_for(levels):
+        for a in ANGLES:
+            got = engine.glcm(img, w, h, levels, [(1, a)], pixel_levels=levels, flags=L.strategy_flag(s))
+            total = O.valid_pair_count(w, h, 1, a)
+            want = np.zeros(levels * levels, dtype=np.uint64)
+            want[v * levels + v] = total
+            assert np.array_equal(got.reshape(-1), want), (s, a)
+
+
+def test_two_tone_spill_both_halves(engine):
+    # cells (255,0), (0,255), (128,128), (200,3) in both u16 halves with heavy counts
+    w, h = 4096, 1024
+    rng = np.random.default_rng(3)
+    base = np.where(rng.random(w * h) < 0.5, 0, 255).astype(np.uint8)
+    base[: w * 300] = 128
+    base[w * 600: w * 700] = np.where(np.arange(w * 100) % 7 == 0, 200, 3)
+    for s in (L.STRAT_PACKED16, L.STRAT_COPY1):
+        got = engine.glcm(base, w, h, 256, [(d, a) for d in (1, 3) for a in ANGLES], pixel_levels=256,
+                          flags=L.strategy_flag(s))
+        for t, (d, a) in enumerate([(d, a) for d in (1, 3) for a in ANGLES]):
+            assert np.array_equal(got[0, t].reshape(-1), O.glcm_serial(base, w, h, 256, d, a)), (s, d, a)
+
+
+def test_quantize_kernel(engine):
+    rng = np.random.default_rng(1)
+    g = rng.integers(0, 256, size=1_000_003, dtype=np.uint8)
+    for levels in (2, 8, 32, 101, 255, 256):
+        assert np.array_equal(engine.quantize(g, levels), O.quantize(g, levels))
+
+
+def _hash_cases(golden_hashes, size, kinds=("noise", "smooth")):
+    return [r for r in golden_hashes["glcm"] if r["size"] == size and r["kind"] in kinds]
+
+
+def _check_hashes(engine, recs):
+    by_img = {}
+    for r in recs:
+        by_img.setdefault((r["kind"], r["size"], r["seed"], r["levels"]), []).append(r)
+    for (kind, n, seed, levels), rs in by_img.items():
+        img = (tf.synth_noise if kind == "noise" else tf.synth_smooth)(n, n, seed).pixels
+        dts = [(r["d"], r["theta"]) for r in rs]
+        got = engine.glcm(img, n, n, levels, dts)
+        for t, r in enumerate(rs):
+            g = got[0, t].reshape(-1)
+            assert O.fnv1a64(g) == r["fnv"], r
+            assert int(g.sum()) == r["total"]
+            best = int(np.argmax(g))
+            assert [best // levels, best % levels] == r["hottest"] and int(g[best]) == r["hottest_votes"]
+
+
+def test_appendix_a_c1_c2(engine, golden_hashes):
+    _check_hashes(engine, _hash_cases(golden_hashes, 512) + _hash_cases(golden_hashes, 4096))
+
+
+@pytest.mark.slow
+def test_appendix_a_c3_and_bands(engine, golden_hashes):
+    _check_hashes(engine, _hash_cases(golden_hashes, 16384) + _hash_cases(golden_hashes, 2048))
+
+
+def test_bands_batch(engine):
+    w, h, nb = 301, 97, 6
+    imgs = [tf.synth_noise(w, h, b + 1).pixels for b in range(nb)]
+    dts = [(1, a) for a in ANGLES] + [(3, 45)]
+    got = engine.glcm(np.concatenate(imgs), w, h, 32, dts, n_bands=nb)
+    for b in range(nb):
+        for t, (d, a) in enumerate(dts):
+            assert np.array_equal(got[b, t].reshape(-1), O.glcm_gray(imgs[b], w, h, 32, d, a)), (b, d, a)
+
+
+def test_host_stream_pipeline_large(engine):
+    # > 32 MiB host image -> the K-chunk copy/compute pipeline (auto K > 1)
+    w, h = 8192, 6000
+    img = tf.synth_noise(w, h, 5).pixels
+    dts = [(1, 0), (2, 45), (4, 90), (1, 135)]
+    got = engine.glcm(img, w, h, 64, dts)
+    for t, (d, a) in enumerate(dts):
+        assert np.array_equal(got[0, t].reshape(-1), O.glcm_gray(img, w, h, 64, d, a))
+
+
+@pytest.mark.parametrize("mode", [tf.ChunkExecution.pipelined, tf.ChunkExecution.sequential])
+def test_chunked_equals_serial_every_k(engine, mode):
+    # mirrors R/tests/test_pipeline.cpp:109-125
+    q = tf.QuantizedImage(37, 29, 8, O.quantize(np.random.default_rng(41).integers(0, 256, 37 * 29,
+                                                                                   dtype=np.uint8), 8))
+    for a in ANGLES:
+        for d in (1, 4):
+            p = tf.GlcmParams(d, tf.Angle(a), 8)
+            want = O.glcm_serial(q.pixels, 37, 29, 8, d, a)
+            for k in (1, 2, 3, 5):
+                if 29 // k <= d and k > 1:
+                    continue
+                g = tf.compute_glcm_chunked(tf.MemoryChunkSource(q), p, tf.plan(8, 49152, 2), k, mode)
+                assert np.array_equal(g.counts, want), (a, d, k)
+
+
+def test_chunked_failure_carries_index(engine):
+    q = tf.QuantizedImage(32, 32, 8, np.random.default_rng(53).integers(0, 8, 1024, dtype=np.uint8))
+
+    class Failing(tf.MemoryChunkSource):
+        def fetch(self, spec, out):
+            if spec.index == 3:
+                raise RuntimeError("simulated source failure")
+            super().fetch(spec, out)
+
+    with pytest.raises(tf.PipelineError) as ei:
+        tf.compute_glcm_chunked(Failing(q), tf.GlcmParams(1, tf.Angle.deg90, 8), tf.plan(8), 8)
+    assert ei.value.chunk_index == 3
+    assert "chunk 3" in str(ei.value)
+    # the engine stays usable after an aborted pipeline
+    g = tf.compute_glcm_chunked(tf.MemoryChunkSource(q), tf.GlcmParams(1, tf.Angle.deg90, 8), tf.plan(8), 8)
+    assert np.array_equal(g.counts, O.glcm_serial(q.pixels, 32, 32, 8, 1, 90))
+
+
+def test_normalize_bit_exact_and_features(engine, small_cases):
+    n = 0
+    for c in small_cases:
+        g = c["counts"]
+        if g.sum() == 0:
+            continue
+        p = engine.normalize(g, c["L"])
+        assert np.array_equal(p.view(np.uint64), c["probs"].view(np.uint64)), c  # bit-exact
+        if not np.isnan(c["feats"]).any():
+            f = engine.features(p, c["L"])
+            assert np.all(np.abs(f - c["feats"]) <= FEAT_TOL * np.maximum(1.0, np.abs(c["feats"]))), (f, c["feats"])
+            n += 1
+    assert n > 100
+
+
+def test_symmetrize_and_fused_post(engine):
+    rng = np.random.default_rng(11)
+    w, h = 211, 123
+    gray = rng.integers(0, 256, size=w * h, dtype=np.uint8)
+    dts = [(1, a) for a in ANGLES]
+    counts, probs, feats = engine.glcm(gray, w, h, 16, dts, flags=L.TFG_SYMMETRIC, want_probs=True,
+                                       want_features=True)
+    for t, (d, a) in enumerate(dts):
+        sym = O.symmetrize(O.glcm_gray(gray, w, h, 16, d, a), 16)
+        assert np.array_equal(counts[0, t].reshape(-1), sym)
+        pr = O.normalize(sym, 16)
+        assert np.array_equal(probs[0, t].reshape(-1).view(np.uint64), pr.view(np.uint64))
+        ft = O.features(pr, 16)
+        assert np.all(np.abs(feats[0, t] - ft) <= FEAT_TOL * np.maximum(1.0, np.abs(ft)))
+
+
+def test_reference_error_behaviour(engine):
+    img = tf.QuantizedImage(4, 4, 8, np.zeros(16, np.uint8))
+    with pytest.raises(ValueError, match="levels do not match"):
+        tf.compute_glcm_serial(img, tf.GlcmParams(1, tf.Angle.deg0, 16))
+    with pytest.raises(ValueError, match="degenerate geometry"):
+        tf.compute_glcm_serial(img, tf.GlcmParams(4, tf.Angle.deg0, 8))
+    with pytest.raises(ValueError, match="all-zero"):
+        tf.normalize(tf.Glcm(2))
+    with pytest.raises(ValueError, match="not normalized"):
+        tf.extract_features(tf.GlcmProbabilities(2, np.array([0.5, 0.5, 0.5, 0.5])))
+    # raw C ABI: a pre-quantised raster holding a value >= L is rejected
+    bad = np.zeros(64 * 64, np.uint8)
+    bad[64 * 63 + 63] = 9  # bottom-right corner: not an anchor at 45 degrees
+    with pytest.raises(ValueError, match="exceeds gray level"):
+        engine.glcm(bad, 64, 64, 8, [(1, 45)], pixel_levels=8)
+    with pytest.raises(ValueError, match="levels do not match"):
+        engine.glcm(bad, 64, 64, 8, [(1, 45)], pixel_levels=16)
+    with pytest.raises(ValueError, match="angle"):
+        engine.glcm(bad, 64, 64, 8, [(1, 30)])
+
+
+def test_async_device_shards_sum_to_whole(engine):
+    torch = pytest.importorskip("torch")
+    w, h, levels = 1000, 777, 32
+    gray = tf.synth_noise(w, h, 9).pixels
+    pitch = 1008
+    dev = torch.zeros((h, pitch), dtype=torch.uint8, device="cuda")
+    dev[:, :w] = torch.from_numpy(gray.reshape(h, w)).cuda()
+    lib = L.load()
+    stream = torch.cuda.current_stream().cuda_stream
+    for d, a in [(1, 0), (2, 45), (3, 90), (1, 135)]:
+        acc = torch.zeros(levels * levels, dtype=torch.int64, device="cuda")
+        specs = tf.partition(w, h, tf.GlcmParams(d, tf.Angle(a), levels), 4)
+        for s in specs:  # each shard: its rows + halo, votes only its owned anchors
+            base = dev[s.owned_row_start:s.buffer_row_end]
+            L.check(lib.tfg_glcm_async(engine.handle, C.c_void_p(base.data_ptr()), w, s.buffer_rows(), pitch,
+                                       s.owned_rows(), 256, levels, d, a, 0, C.c_void_p(acc.data_ptr()),
+                                       C.c_void_p(stream)))
+        torch.cuda.synchronize()
+        got = acc.cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, O.glcm_gray(gray, w, h, levels, d, a)), (d, a)
+    L.check(lib.tfg_check_async_errors(engine.handle))

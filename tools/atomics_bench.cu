@@ -1,0 +1,99 @@
+// atomics_bench.cu — sm_100a microbenchmark of shared-memory vote primitives.
+// Decides the K1 vote strategy per L by measurement:
+// throughput of ATOMS.ADD / ATOMS.POPC.INC / LDS+STS under the address
+// patterns a GLCM vote produces. Prints one JSON object.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdint>
+
+constexpr int kT = 1024;
+constexpr int kIters = 4096;
+
+enum Mode {
+  M_LANE_PRIVATE_INC = 0,   // [cell][lane] layout, add 1           (COPIES32 on noise)
+  M_LANE_PRIVATE_ADDN,      // same, add variable n
+  M_RANDOM_64K_INC,         // random word in 128 KB (L=256 packed / L=181 u32)
+  M_RANDOM_64K_RET,         // same, with return value consumed (PACKED16 spill check)
+  M_RANDOM_4K_INC,          // random word in 16 KB (L=64, R=1)
+  M_SAME_ADDR_INC,          // all lanes of a warp on one word (smooth hot cell, R=1)
+  M_SAME_ADDR_ADDN,         // same, variable increment
+  M_LDS_STS_PRIVATE,        // non-atomic RMW, lane-private
+  M_RANDOM_8WAY,            // COPIES8 layout: random cell*8 + lane%8 over 16K words
+  M_NMODES
+};
+const char* kNames[] = {"lane_private_inc", "lane_private_addn", "random_128KB_inc", "random_128KB_ret",
+                        "random_16KB_inc", "same_addr_inc", "same_addr_addn", "lds_sts_private",
+                        "copies8_random"};
+
+template <int mode>
+__global__ void __launch_bounds__(kT, 1) bench(unsigned long long* cycles, uint32_t* sink) {
+  extern __shared__ uint32_t s[];
+  for (int i = threadIdx.x; i < 32768; i += kT) s[i] = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t acc = 0;
+  uint32_t h = threadIdx.x * 0x9E3779B9u + blockIdx.x * 0x85EBCA6Bu;
+  const unsigned long long t0 = clock64();
+#pragma unroll 8
+  for (int k = 0; k < kIters; ++k) {
+    h = h * 1664525u + 1013904223u;  // LCG, 1 IMAD
+    const uint32_t r = h >> 9;
+    switch (mode) {  // compile-time
+      case M_LANE_PRIVATE_INC: atomicAdd(&s[((r & 1023) << 5) | lane], 1u); break;
+      case M_LANE_PRIVATE_ADDN: atomicAdd(&s[((r & 1023) << 5) | lane], (h & 7) + 1); break;
+      case M_RANDOM_64K_INC: atomicAdd(&s[r & 32767], 1u); break;
+      case M_RANDOM_64K_RET: acc += atomicAdd(&s[r & 32767], 1u << ((h >> 3) & 16)); break;
+      case M_RANDOM_4K_INC: atomicAdd(&s[r & 4095], 1u); break;
+      case M_SAME_ADDR_INC: atomicAdd(&s[(warp << 5) | (k & 31)], 1u); break;
+      case M_SAME_ADDR_ADDN: atomicAdd(&s[(warp << 5) | (k & 31)], (lane & 3) + 1); break;
+      case M_LDS_STS_PRIVATE: {
+        volatile uint32_t* v = s;
+        const uint32_t a = ((r & 1023) << 5) | lane;
+        v[a] = v[a] + 1;
+        break;
+      }
+      case M_RANDOM_8WAY: atomicAdd(&s[((r & 4095) << 3) | (lane & 7)], 1u); break;
+    }
+  }
+  const unsigned long long t1 = clock64();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(cycles, t1 - t0);
+  if (acc == 0x12345678u) sink[0] = acc + s[lane];
+}
+
+int main() {
+  int dev = 0, sms = 0, clk = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+  unsigned long long* cyc;
+  uint32_t* sink;
+  cudaMalloc(&cyc, 8);
+  cudaMalloc(&sink, 64);
+  using K = void (*)(unsigned long long*, uint32_t*);
+  K ks[M_NMODES] = {bench<0>, bench<1>, bench<2>, bench<3>, bench<4>, bench<5>, bench<6>, bench<7>, bench<8>};
+  for (auto k : ks) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  printf("{\"sms\": %d, \"clock_khz\": %d, \"modes\": {", sms, clk);
+  for (int m = 0; m < M_NMODES; ++m) {
+    for (int rep = 0; rep < 2; ++rep) {  // first rep = warm-up
+      cudaMemset(cyc, 0, 8);
+      cudaEventRecord(a);
+      ks[m]<<<sms, kT, 131072>>>(cyc, sink);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    unsigned long long c = 0;
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    const double ops = (double)sms * kT * kIters;
+    printf("%s\"%s\": {\"ms\": %.4f, \"Gops_s\": %.1f, \"ops_per_clk_per_sm\": %.3f, \"sm_mhz_est\": %.0f}",
+           m ? ", " : "", kNames[m], ms, ops / ms / 1e6, (double)kT * kIters / (double)c, c / (ms * 1e3));
+  }
+  printf("}, \"err\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
