@@ -69,31 +69,51 @@ def make_images(tf, n, kinds, n_bands, rank):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled DURING the timed region (NVML every
+    ~2 ms; nvidia-smi as fallback)."""
+    # nvmlClocksEventReason* bits
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, reasons_mask)
+        self.sm_max = None
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.sm_max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml:
+            n = self._nvml
+            return (n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM),
+                    n.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+        sm, mx = [float(x) for x in out.strip().split(",")]
+        self.sm_max = mx
+        return (sm, 0)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.002)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.01)
         return self
 
     def __exit__(self, *a):
@@ -102,14 +122,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
-                          and "Not" not in s[2 + i]})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.sm_max, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples]
+        reasons = sorted({name for _, m in self.samples for bit, name in self.REASONS.items() if m & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.sm_max, "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def hbm_peak():
@@ -300,6 +317,16 @@ def run_engine(args, wl):
 
     # end-to-end through the public API from pinned host memory
     pinned = {k: torch.from_numpy(v).pin_memory() for k, v in imgs.items()}
+    probe = torch.empty(pinned[kinds[0]].numel(), dtype=torch.uint8, device="cuda")
+    h2d_gbs = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        probe.copy_(pinned[kinds[0]], non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        h2d_gbs.append(probe.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    del probe
     e2e_steps = max(2, min(args.steps, 10))
     h2d = sum(v.numel() for v in pinned.values())
     d2h = n_out * cells * 8
@@ -345,7 +372,9 @@ def run_engine(args, wl):
                          "kernel": "glcm_vote_kernel (+ glcm_reduce_partials_kernel for L*L > 4096)",
                          "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "tfg_glcm (host pinned input, Scheme-3 stream pipeline, counts to host)"},
+                    "api": "tfg_glcm (host pinned input, Scheme-3 stream pipeline, counts to host)",
+                    "pinned_h2d_GBps": max(h2d_gbs), "ms_per_step": e2e_s * 1e3,
+                    "h2d_bound_ms_per_step": h2d / (max(h2d_gbs) * 1e9) * 1e3},
             "gpu_launches": gpu_launches,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

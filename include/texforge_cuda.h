@@ -151,7 +151,7 @@ int tfg_features(tfg_ctx* ctx, const double* probs, int levels, double* out5);
 /*
  * Device-resident asynchronous entry (no host sync): ADDS the GLCM of one
  * (d, theta) of a device image into d_counts (L*L u64, device) on `stream`
- * (a cudaStream_t; NULL = the context's exec stream). `row_end` limits the
+ * (a cudaStream_t; NULL = the legacy default stream, as in CUDA). `row_end` limits the
  * anchor rows (the owned rows of a shard; pass height for the whole image):
  * rows [row_end, height) are read-only halo, exactly like a ChunkSpec.
  * Used by the benchmark, the multi-GPU row shards and the parity tests.

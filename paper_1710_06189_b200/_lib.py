@@ -34,8 +34,10 @@ def strategy_flag(s: int) -> int:
     return (int(s) & 0xF) << TFG_STRATEGY_SHIFT
 
 
+# `err` is a raw char* the callback may write into (NOT c_char_p: ctypes would
+# hand Python an immutable bytes copy).
 FETCH_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t,
-                       C.POINTER(C.c_uint8), C.c_char_p, C.c_size_t)
+                       C.POINTER(C.c_uint8), C.c_void_p, C.c_size_t)
 
 # (name, restype, argtypes) for every symbol declared in include/texforge_cuda.h
 _u8p = C.POINTER(C.c_uint8)

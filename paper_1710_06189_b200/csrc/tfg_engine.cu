@@ -236,30 +236,27 @@ VoteKernel pick_global(int quant, int ksel) {
   }
 }
 
-struct KernelInfo {
-  VoteKernel fn = nullptr;
-  int smem_set = -1;
-  int blocks_per_sm = 0;
-};
+// Every vote kernel gets the full 227 KB dynamic shared-memory opt-in once;
+// occupancy is then queried per (kernel, smem) pair.
 std::mutex g_kinfo_mu;
-std::vector<std::pair<VoteKernel, KernelInfo>> g_kinfo;
+std::vector<VoteKernel> g_kopted;
+std::vector<std::pair<std::pair<VoteKernel, size_t>, int>> g_kocc;
 
 int occupancy_for(VoteKernel fn, size_t smem) {
   std::lock_guard<std::mutex> lk(g_kinfo_mu);
-  for (auto& e : g_kinfo)
-    if (e.first == fn && e.second.smem_set == (int)smem) return e.second.blocks_per_sm;
-  ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)std::max<size_t>(smem, 0)),
-     "cudaFuncSetAttribute");
+  for (auto& e : g_kocc)
+    if (e.first.first == fn && e.first.second == smem) return e.second;
+  if (std::find(g_kopted.begin(), g_kopted.end(), fn) == g_kopted.end()) {
+    ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            227 * 1024),
+       "cudaFuncSetAttribute");
+    g_kopted.push_back(fn);
+  }
   int bps = 0;
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, reinterpret_cast<const void*>(fn), tfg::kThreads, smem),
      "occupancy");
   if (bps < 1) fail(TFG_CUDA_ERROR, "vote kernel cannot be resident (shared memory / registers)");
-  KernelInfo ki;
-  ki.fn = fn;
-  ki.smem_set = (int)smem;
-  ki.blocks_per_sm = bps;
-  g_kinfo.push_back({fn, ki});
+  g_kocc.push_back({{fn, smem}, bps});
   return bps;
 }
 
@@ -895,7 +892,7 @@ int tfg_glcm_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t heigh
       fail(TFG_INVALID_ARGUMENT, "glcm_async: device image must be 16-byte aligned with pitch % 16 == 0");
     if (row_end > height) fail(TFG_INVALID_ARGUMENT, "glcm_async: row_end > height");
     DeviceGuard dg(ctx->device);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->exec;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
     if (pixel_levels == levels) launch_validate(ctx, d_px, width, height, pitch, 0, 1, levels, ctx->d_err, s);
     launch_vote(ctx, d_px, width, height, pitch, 0, 1, row_end, pixel_levels, levels, distance, angle_deg, flags,
                 reinterpret_cast<unsigned long long*>(d_counts), s);
@@ -908,7 +905,7 @@ int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned 
   return guarded([&] {
     check_levels(levels, "Glcm");
     DeviceGuard dg(ctx->device);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->exec;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
     const size_t cells = (size_t)levels * levels;
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(d_counts);
     if ((flags & TFG_SYMMETRIC) && d_sym_out) {

@@ -317,8 +317,9 @@ class Engine:
                 return 0
             except BaseException as e:  # noqa: BLE001 — any source failure aborts the pipeline
                 err_box["exc"] = e
-                msg = str(e).encode()[: max(0, err_len - 1)]
-                C.memmove(err, msg, len(msg))
+                msg = str(e).encode()[: max(0, int(err_len) - 1)] + b"\0"
+                if err:
+                    C.memmove(err, msg, len(msg))
                 return 1
 
         cb = L.FETCH_FN(_fetch)
