@@ -289,6 +289,7 @@ VoteGeometry make_geometry(size_t width, size_t height, size_t pitch, size_t row
   const long rem = dc - qq * 16;  // 0..15
   g.ksel = rem == 0 ? 4 : (int)(rem >> 2);
   p.sbits = (int)((rem & 3) * 8);
+  p.ref_off = (long long)dr * (long long)pitch + p.qoff;
   p.col_begin = dc < 0 ? (int)d : 0;
   p.col_end = dc > 0 ? (int)(width - d) : (int)width;
   const long row_limit = (long)height - dr;
@@ -355,7 +356,7 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   // persistent-style grid: at most one wave of CTAs per band set, and no CTA
   // with less than one round of work.
   long long per_band = std::max<long long>(1, (long long)ctx->num_sms * bps / std::max(n_bands, 1));
-  per_band = std::min<long long>(per_band, (p.items + tfg::kRoundItems - 1) / tfg::kRoundItems);
+  per_band = std::min<long long>(per_band, (p.items + 2 * tfg::kThreads - 1) / (2 * tfg::kThreads));
   per_band = std::max<long long>(per_band, 1);
   p.items_per_cta = (p.items + per_band - 1) / per_band;
   const bool use_partials = cells > 4096;

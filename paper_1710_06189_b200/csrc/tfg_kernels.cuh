@@ -48,6 +48,7 @@ struct VoteParams {
   int levels;
   int dr;                           // row displacement (>= 0)
   int qoff;                         // 16*floor(dcol/16)
+  long long ref_off;                // drow*pitch + qoff: anchor segment -> first reference segment
   int sbits;                        // 8*(dcol mod 4)
   int col_begin, col_end;           // valid anchor columns
   int ch0, nch;                     // first 16-px chunk, chunks per row
@@ -146,40 +147,55 @@ __device__ __forceinline__ uint4 ldg16(const uint8_t* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }
 
-// Loads one item's anchor segment A and the 16 reference bytes R.
-// KSEL 0..3: word shift k of the displacement; KSEL 4: byte-aligned (dcol%16==0).
+// The three 16-byte loads of one item (anchor segment + the two aligned
+// segments that contain its reference bytes) and its valid-anchor mask.
+struct RawItem {
+  uint4 a, c0, c1;
+  uint32_t mask;
+};
+
+// Issues the loads of item (row, j). Interior segments (0 < j < nch-1) need no
+// bounds logic: every reference byte of an interior segment lies inside the
+// row, so only the two edge segments of a row pay for masks.
 template <int KSEL>
-__device__ __forceinline__ void load_item(const VoteParams& p, const uint8_t* band, long long row,
-                                          int j, bool live, uint32_t (&A)[4], uint32_t (&R)[4],
-                                          uint32_t& mask) {
-  const int col0 = (p.ch0 + j) * 16;
-  mask = 0;
-  if (!live) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) A[i] = R[i] = 0;
+__device__ __forceinline__ void issue_item(const VoteParams& p, const uint8_t* band, long long row, int j,
+                                           bool live, RawItem& it) {
+  it.a = it.c0 = it.c1 = make_uint4(0, 0, 0, 0);
+  it.mask = 0;
+  if (!live) return;
+  const int col0 = (p.ch0 + j) << 4;
+  const uint8_t* ap = band + (unsigned long long)row * p.pitch + col0;
+  const uint8_t* rp = ap + p.ref_off;
+  it.a = ldg16(ap);
+  if (j > 0 && j < p.nch - 1) {
+    it.mask = 0xFFFFu;
+    it.c0 = ldg16(rp);
+    if constexpr (KSEL != 4) it.c1 = ldg16(rp + 16);
     return;
   }
   const int lo = p.col_begin - col0;
   const int hi = p.col_end - col0;
-  mask = 0xFFFFu;
-  if (lo > 0) mask &= 0xFFFFu << lo;
-  if (hi < 16) mask &= (1u << hi) - 1u;
-
-  const uint8_t* arow = band + (unsigned long long)row * p.pitch;
-  const uint8_t* rrow = arow + (unsigned long long)p.dr * p.pitch;
-  const uint4 a = ldg16(arow + col0);
-  A[0] = a.x; A[1] = a.y; A[2] = a.z; A[3] = a.w;
-
+  uint32_t m = 0xFFFFu;
+  if (lo > 0) m &= 0xFFFFu << lo;
+  if (hi < 16) m &= (1u << hi) - 1u;
+  it.mask = m;
   const long long cs = (long long)col0 + p.qoff;
   const long long pitch = (long long)p.pitch;
-  uint4 c0 = make_uint4(0, 0, 0, 0);
-  if (cs >= 0 && cs < pitch) c0 = ldg16(rrow + cs);
+  if (cs >= 0 && cs < pitch) it.c0 = ldg16(rp);
+  if constexpr (KSEL != 4) {
+    if (cs + 16 >= 0 && cs + 16 < pitch) it.c1 = ldg16(rp + 16);
+  }
+}
+
+// Reference bytes R[0..3] of an item: bytes [4k+s, 4k+s+16) of c0:c1.
+template <int KSEL>
+__device__ __forceinline__ void ref_words(const VoteParams& p, const RawItem& it, uint32_t (&A)[4],
+                                          uint32_t (&R)[4]) {
+  A[0] = it.a.x; A[1] = it.a.y; A[2] = it.a.z; A[3] = it.a.w;
   if constexpr (KSEL == 4) {
-    R[0] = c0.x; R[1] = c0.y; R[2] = c0.z; R[3] = c0.w;
+    R[0] = it.c0.x; R[1] = it.c0.y; R[2] = it.c0.z; R[3] = it.c0.w;
   } else {
-    uint4 c1 = make_uint4(0, 0, 0, 0);
-    if (cs + 16 >= 0 && cs + 16 < pitch) c1 = ldg16(rrow + cs + 16);
-    const uint32_t W[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const uint32_t W[8] = {it.c0.x, it.c0.y, it.c0.z, it.c0.w, it.c1.x, it.c1.y, it.c1.z, it.c1.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) R[i] = __funnelshift_r(W[i + KSEL], W[i + KSEL + 1], p.sbits);
   }
@@ -201,6 +217,8 @@ __device__ __forceinline__ void cells_of(const VoteParams& p, const uint32_t (&A
 
 // ---------------------------------------------------------------------------
 // K1 + K2: fused quantise, vote, privatised merge.
+// Each thread walks items tid, tid+1024, ... of its CTA's contiguous item
+// range, with the NEXT item's loads in flight while the current one votes.
 template <int QUANT, int STRAT, int KSEL>
 __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams p) {
   extern __shared__ __align__(16) uint32_t hist[];
@@ -216,7 +234,6 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     const int n4 = p.hist_words >> 2;
     for (int i = tid; i < n4; i += kThreads) h4[i] = make_uint4(0, 0, 0, 0);
   }
-  __syncthreads();
 
   uint32_t* h = hist;
   if constexpr (STRAT == S_COPIES32) h += lane;
@@ -226,36 +243,31 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   long long end = start + p.items_per_cta;
   if (end > p.items) end = p.items;
 
+  long long row = 0;
+  int j = 0;
+  RawItem nxt;
   if (start < end) {
-    long long item = start + tid;
-    long long row = item / p.nch;
-    int j = (int)(item - row * p.nch);
-    for (long long base = start; base < end; base += kRoundItems) {
-      // item 0 = (row, j); item 1 = item 0 + kThreads
-      long long row1 = row + p.step_r;
-      int j1 = j + p.step_j;
-      if (j1 >= p.nch) { j1 -= p.nch; ++row1; }
-      const bool live0 = base + tid < end;
-      const bool live1 = base + kThreads + tid < end;
+    const long long item = start + tid;
+    row = item / p.nch;
+    j = (int)(item - row * p.nch);
+    issue_item<KSEL>(p, band, row, j, item < end, nxt);
+  }
+  __syncthreads();  // histogram zeroed
 
-      uint32_t A0[4], R0[4], A1[4], R1[4], m0, m1;
-      load_item<KSEL>(p, band, row, j, live0, A0, R0, m0);
-      load_item<KSEL>(p, band, row1, j1, live1, A1, R1, m1);
-      {
-        uint32_t E[4], O[4];
-        cells_of<QUANT, STRAT>(p, A0, R0, E, O);
-        vote16<STRAT>(h, E, O, m0, glcm);
-      }
-      {
-        uint32_t E[4], O[4];
-        cells_of<QUANT, STRAT>(p, A1, R1, E, O);
-        vote16<STRAT>(h, E, O, m1, glcm);
-      }
-      if constexpr (STRAT == S_PACKED16) __syncthreads();  // <= 32768 votes per round
-      // advance item 0 by 2*kThreads
-      row = row1 + p.step_r;
-      j = j1 + p.step_j;
-      if (j >= p.nch) { j -= p.nch; ++row; }
+  int it = 0;
+  for (long long base = start; base < end; base += kThreads, ++it) {
+    const RawItem cur = nxt;
+    row += p.step_r;
+    j += p.step_j;
+    if (j >= p.nch) { j -= p.nch; ++row; }
+    issue_item<KSEL>(p, band, row, j, base + kThreads + tid < end, nxt);  // prefetch
+    uint32_t A[4], R[4], E[4], O[4];
+    ref_words<KSEL>(p, cur, A, R);
+    cells_of<QUANT, STRAT>(p, A, R, E, O);
+    vote16<STRAT>(h, E, O, cur.mask, glcm);
+    // PACKED16: <= 2 x 16384 votes per CTA between barriers (spill invariant)
+    if constexpr (STRAT == S_PACKED16) {
+      if (it & 1) __syncthreads();
     }
   }
   __syncthreads();
@@ -318,9 +330,12 @@ __global__ void glcm_vote_global_kernel(const VoteParams p) {
        item += (long long)gridDim.x * blockDim.x) {
     const long long row = item / p.nch;
     const int j = (int)(item - row * p.nch);
-    uint32_t A[4], R[4], m, E[4], O[4];
-    load_item<KSEL>(p, band, row, j, true, A, R, m);
+    RawItem ri;
+    issue_item<KSEL>(p, band, row, j, true, ri);
+    uint32_t A[4], R[4], E[4], O[4];
+    ref_words<KSEL>(p, ri, A, R);
     cells_of<QUANT, S_COPY1>(p, A, R, E, O);
+    const uint32_t m = ri.mask;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (m & (1u << (4 * i + 0))) atomicAdd(glcm + (E[i] & 0xFFFFu), 1ull);
