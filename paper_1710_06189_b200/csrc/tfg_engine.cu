@@ -35,6 +35,7 @@ struct Failure {
 
 void ck(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return;
+  cudaGetLastError();  // clear a non-sticky error so it is not re-reported by the next launch check
   if (e == cudaErrorMemoryAllocation) fail(TFG_OUT_OF_MEMORY, std::string(what) + ": out of device memory");
   fail(TFG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -159,31 +160,32 @@ void check_geometry(size_t width, size_t height, int distance) {
     fail(TFG_INVALID_ARGUMENT, "glcm: degenerate geometry (d must be in [1, min(width, height)))");
 }
 
+// 227 KB opt-in per CTA minus the kernel's static shared memory and slack.
+constexpr size_t kMaxHistBytes = 227 * 1024 - 256;
+
 int pick_strategy(int levels, unsigned flags) {
   const int forced = (int)((flags >> TFG_STRATEGY_SHIFT) & 0xF);
-  const size_t cells = (size_t)levels * levels;
   if (forced) {
-    const bool ok = (forced == TFG_STRAT_COPIES32 && cells * 128 <= 227 * 1024) ||
-                    (forced == TFG_STRAT_COPIES8 && cells * 32 <= 227 * 1024) ||
-                    (forced == TFG_STRAT_COPY1 && cells * 4 <= 227 * 1024) ||
-                    (forced == TFG_STRAT_PACKED16);
-    if (!ok) fail(TFG_INVALID_ARGUMENT, "strategy does not fit shared memory for these levels");
+    const bool ok = (forced == TFG_STRAT_COPIES32 && levels <= 32) || (forced == TFG_STRAT_COPIES8 && levels <= 64) ||
+                    (forced == TFG_STRAT_COPY1 && levels <= 128) || (forced == TFG_STRAT_PACKED16);
+    if (!ok) fail(TFG_INVALID_ARGUMENT, "strategy does not support these levels");
     return forced;
   }
   if (levels <= 32) return tfg::S_COPIES32;
   if (levels <= 64) return tfg::S_COPIES8;
-  if (cells * 4 <= 227 * 1024) return tfg::S_COPY1;
+  if (levels <= 128) return tfg::S_COPY1;
   return tfg::S_PACKED16;
 }
 
+// Shared-memory words of a strategy's layout (tfg_kernels.cuh, enum Strat).
 size_t hist_words_of(int strat, int levels) {
-  const size_t cells = (size_t)levels * levels;
+  const size_t L = (size_t)levels;
   size_t w = 0;
   switch (strat) {
-    case tfg::S_COPIES32: w = cells * 32; break;
-    case tfg::S_COPIES8: w = cells * 8; break;
-    case tfg::S_COPY1: w = cells; break;
-    default: w = std::min<size_t>(cells, 32768); break;
+    case tfg::S_COPIES32: w = L * 32 * 32; break;   // cells a + 32b, 32 copies
+    case tfg::S_COPIES8: w = L * 64 * 8; break;     // cells b + 64a, 8 copies
+    case tfg::S_COPY1: w = L * 128; break;          // cells a + 128b
+    default: w = std::min<size_t>(L * 256, 32768); break;  // words (a + 256b) & 0x7fff
   }
   return (w + 3) & ~size_t(3);
 }
@@ -247,8 +249,13 @@ int occupancy_for(VoteKernel fn, size_t smem) {
   for (auto& e : g_kocc)
     if (e.first.first == fn && e.first.second == smem) return e.second;
   if (std::find(g_kopted.begin(), g_kopted.end(), fn) == g_kopted.end()) {
+    int dev = 0, optin = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
+    cudaFuncAttributes fa{};
+    ck(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)), "cudaFuncGetAttributes");
     ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            227 * 1024),
+                            optin - (int)fa.sharedSizeBytes),
        "cudaFuncSetAttribute");
     g_kopted.push_back(fn);
   }
@@ -298,15 +305,29 @@ VoteGeometry make_geometry(size_t width, size_t height, size_t pitch, size_t row
   p.ch0 = p.col_begin / 16;
   p.nch = (p.col_end + 15) / 16 - p.ch0;
   p.items = (long long)nrows * p.nch;
+  if (p.items >= (1ll << 31))
+    fail(TFG_INVALID_ARGUMENT, "glcm: image too large for one launch (>= 2^31 16-pixel segments); split it into chunks");
   g.empty = p.items == 0 || p.col_end <= p.col_begin;
-  p.step_r = tfg::kThreads / std::max(p.nch, 1);
-  p.step_j = tfg::kThreads % std::max(p.nch, 1);
+  {
+    // CUTLASS-style FastDivmod constants: q = umulhi(n, mul) >> shr for n < 2^31
+    const uint32_t dv = (uint32_t)std::max(p.nch, 1);
+    if (dv == 1) {
+      p.div_mul = 0;
+      p.div_shr = 0;
+    } else {
+      uint32_t l = 0;
+      while ((1ull << l) < dv) ++l;  // ceil(log2 d)
+      const uint32_t pw = 31 + l;
+      p.div_mul = (uint32_t)(((1ull << pw) + dv - 1) / dv);
+      p.div_shr = pw - 32;
+    }
+  }
   // quantisation mode
   (void)pixel_levels;
   return g;
 }
 
-int quant_mode(int pixel_levels, int levels, uint32_t* mask, int* shift) {
+int quant_mode(int pixel_levels, int levels, uint32_t* mask, int* shift, int* lgp = nullptr) {
   *mask = 0;
   *shift = 0;
   if (levels == 256) return tfg::Q_NONE;
@@ -319,6 +340,7 @@ int quant_mode(int pixel_levels, int levels, uint32_t* mask, int* shift) {
     while ((1 << lg) < levels) ++lg;
     *shift = 8 - lg;
     *mask = (uint32_t)(levels - 1) * 0x01010101u;
+    if (lgp) *lgp = lg;
     return tfg::Q_SHIFT;
   }
   return tfg::Q_MUL;
@@ -334,7 +356,13 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   p.img = d_img;
   p.band_stride = band_stride;
   p.glcm = d_glcm;
-  const int quant = quant_mode(pixel_levels, levels, &p.qmask, &p.qshift);
+  int lg = 0;
+  const int quant = quant_mode(pixel_levels, levels, &p.qmask, &p.qshift, &lg);
+  if (quant == tfg::Q_SHIFT && !(flags & TFG_SCHEME_GLOBAL)) {
+    // the scaled side of a layout: ((v >> s) & m) << sc == (v >> (s - sc)) & (m << sc); s >= sc
+    // holds because each layout is only used for L <= 2^(8 - sc).
+    p.qshift_scaled = p.qshift - tfg::strat_scale(pick_strategy(levels, flags));
+  }
   const size_t cells = (size_t)levels * levels;
 
   if (flags & TFG_SCHEME_GLOBAL) {

@@ -11,21 +11,25 @@
 // K3 symmetrize / normalize, K4 features — post-processing on device.
 //
 // Work decomposition: the valid-anchor raster is cut into
-// 16-pixel "items" (one 16-byte vector per row segment).  A CTA of 1024
-// threads owns a contiguous item range and walks it in rounds of 2 items per
-// thread; consecutive threads take consecutive 16-byte segments of a row, so
-// every LDG.128 of a warp is one coalesced 512-byte access.  The reference
+// 16-pixel "items" (one 16-byte vector per row segment). A warp takes batches
+// of 32 consecutive items (one per lane: every LDG.128 of the warp is one
+// coalesced 512-byte access) from a per-CTA ticket counter and keeps three
+// batches in a register ring (two in flight while one votes). The reference
 // neighbour of each segment is two aligned 16-byte loads + funnel shifts
-// (displacement dcol = 16q + 4k + s: q and the word shift k are template /
-// launch constants, s is a byte funnel shift).
+// (displacement dcol = 16q + 4k + s: q and the word shift k are launch /
+// template constants, s is a byte funnel shift).
+//
+// The vote itself is 3 instructions: the quantised anchor and reference bytes
+// are pre-scaled so that ONE byte permute (PRMT) of an anchor word and a
+// reference word gives a pixel pair's shared-memory offset, then one IMAD adds
+// the lane's copy base and one red.shared.add casts the vote.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace tfg {
 
-constexpr int kThreads = 1024;   // threads per vote CTA
-constexpr int kRoundItems = 2 * kThreads;
+constexpr int kThreads = 768;  // threads per vote CTA (24 warps: 85 regs for the 3-slot ring)
 
 enum Quant : int {
   Q_NONE = 0,   // values used as-is (gray with L=256, or quantised with L=256)
@@ -34,12 +38,20 @@ enum Quant : int {
   Q_MUL = 3     // gray input, any L:   q = (v*L) >> 8       (image.hpp:55-62)
 };
 
+// Privatised sub-GLCM layouts. x = PRMT(P, Q) = P_byte + 256*Q_byte per pixel.
 enum Strat : int {
-  S_COPIES32 = 1,  // 32 u32 copies, interleaved [cell][lane]: bank = lane, conflict-free
-  S_COPIES8 = 2,   // 8 u32 copies interleaved [cell][lane%8]
-  S_COPY1 = 3,     // one u32 copy
-  S_PACKED16 = 4   // one copy of u16 counters, two per word, exact spill at 2^15
+  S_COPIES32 = 1,  // L <= 32:  32 u32 copies [a + 32b][lane]; P = 8a, Q = b, addr = 16x + 4 lane
+  S_COPIES8 = 2,   // L <= 64:  8 u32 copies [b + 64a][lane%8]; P = 4b, Q = a, addr = 8x + 4 (lane%8)
+  S_COPY1 = 3,     // L <= 128: 1 u32 copy [a + 128b]; P = 2a, Q = b, addr = 2x
+  S_PACKED16 = 4   // L <= 256: 1 copy of u16 counters, cell a + 256b in word (x & 0x7fff), half b >> 7
 };
+
+__host__ __device__ constexpr int strat_scale(int s) {  // log2 of the P-byte scale
+  return s == S_COPIES32 ? 3 : (s == S_COPIES8 ? 2 : (s == S_COPY1 ? 1 : 0));
+}
+__host__ __device__ constexpr int strat_copies(int s) {
+  return s == S_COPIES32 ? 32 : (s == S_COPIES8 ? 8 : 1);
+}
 
 struct VoteParams {
   const uint8_t* img;               // band 0, 16-byte aligned
@@ -55,9 +67,10 @@ struct VoteParams {
   int nrows;                        // anchor rows [0, nrows)
   long long items;                  // nrows*nch (per band)
   long long items_per_cta;
-  int step_r, step_j;               // (kThreads / nch, kThreads % nch)
-  uint32_t qmask;                   // Q_SHIFT / Q_CLAMP per-byte mask
-  int qshift;                       // Q_SHIFT
+  uint32_t div_mul, div_shr;        // fast division by nch (div_mul == 0: nch == 1)
+  uint32_t qmask;                   // Q_SHIFT / Q_CLAMP per-byte mask (L-1)*0x01010101
+  int qshift;                       // Q_SHIFT: s = 8 - log2 L
+  int qshift_scaled;                // Q_SHIFT: s - strat_scale
   int hist_words;                   // shared-memory words
   unsigned long long* glcm;         // band b accumulator at glcm + b*L*L
   uint32_t* partials;               // null -> direct u64 atomics; else [band][grid][L*L]
@@ -81,72 +94,159 @@ __device__ __forceinline__ uint32_t quant4(uint32_t w, const VoteParams& p) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// one vote of weight n into the privatised sub-GLCMs
-template <int STRAT>
-__device__ __forceinline__ void emit(uint32_t* h, uint32_t cell, uint32_t n,
-                                     unsigned long long* glcm) {
-  if constexpr (STRAT == S_COPIES32) {
-    atomicAdd(h + cell * 32u, n);
-  } else if constexpr (STRAT == S_COPIES8) {
-    atomicAdd(h + cell * 8u, n);
-  } else if constexpr (STRAT == S_COPY1) {
-    atomicAdd(h + cell, n);
+// Quantised bytes of 4 pixels, times 2^sc (bytes stay < 256: no byte carry).
+template <int QUANT, int SC>
+__device__ __forceinline__ uint32_t quant4_scaled(uint32_t w, const VoteParams& p) {
+  if constexpr (SC == 0) {
+    return quant4<QUANT>(w, p);
+  } else if constexpr (QUANT == Q_SHIFT) {
+    return (w >> p.qshift_scaled) & (p.qmask << SC);  // ((w >> s) & m) << sc in two ops
   } else {
-    // cell c lives in word (c & 0x7fff), half (c >> 15).  A field never
-    // wraps: every CTA round adds <= 32768 to the CTA's counters and every
-    // field is < 0x8000 at a round boundary, so a field crossing 0x7fff ->
-    // 0x8000 is seen by exactly one atomic (its bit 15 flips 0 -> 1), whose
-    // thread moves 0x8000 votes to the global u64 cell before the barrier.
-    const uint32_t sh = (cell >> 11) & 16u;
-    const uint32_t inc = n << sh;
-    uint32_t* w = h + (cell & 0x7fffu);
-    const uint32_t old = atomicAdd(w, inc);
-    if ((~old & (old + inc)) & 0x80008000u) {
-      atomicAdd(w, 0u - (0x8000u << sh));
-      atomicAdd(glcm + cell, 0x8000ull);
+    return quant4<QUANT>(w, p) << SC;
+  }
+}
+
+// P/Q words of an item: PRMT(P[i], Q[i]) byte j = offset of pixel 4i+j.
+template <int QUANT, int STRAT>
+__device__ __forceinline__ void prep_words(const VoteParams& p, const uint32_t (&A)[4], const uint32_t (&R)[4],
+                                           uint32_t (&P)[4], uint32_t (&Q)[4]) {
+  constexpr int sc = strat_scale(STRAT);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if constexpr (STRAT == S_COPIES8) {  // reference side scaled, anchor-major cells
+      P[i] = quant4_scaled<QUANT, sc>(R[i], p);
+      Q[i] = quant4<QUANT>(A[i], p);
+    } else {
+      P[i] = quant4_scaled<QUANT, sc>(A[i], p);
+      Q[i] = quant4<QUANT>(R[i], p);
     }
   }
 }
 
-// E[i] holds the cells of pixels 4i, 4i+2 (u16 lanes); O[i] of 4i+1, 4i+3.
+// byte j of P in bits 0-7, byte j of Q in bits 8-15, bits 16-31 = sign of Q
+// byte 0 (zero: every Q byte of a non-packed layout is < 128).
+__device__ __forceinline__ uint32_t pair_x(uint32_t P, uint32_t Q, int j) {
+  return __byte_perm(P, Q, 0xCC00u | ((4u + j) << 4) | (uint32_t)j);
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory votes on 32-bit shared addresses
+__device__ __forceinline__ void red_smem(uint32_t addr, uint32_t n) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(n) : "memory");
+}
+__device__ __forceinline__ void red_smem1(uint32_t addr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_smem(uint32_t addr, uint32_t n) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(n) : "memory");
+  return old;
+}
+
 template <int STRAT>
-__device__ __forceinline__ void vote16(uint32_t* h, const uint32_t (&E)[4], const uint32_t (&O)[4],
-                                       uint32_t mask, unsigned long long* glcm) {
+__device__ __forceinline__ uint32_t vote_addr(uint32_t hb, uint32_t x) {
+  if constexpr (STRAT == S_COPIES32) return x * 16u + hb;
+  else if constexpr (STRAT == S_COPIES8) return x * 8u + hb;
+  else if constexpr (STRAT == S_COPY1) return x * 2u + hb;
+  else return (x & 0x7fffu) * 4u + hb;
+}
+
+// PACKED16 increment for pixel j of word Q: 1 or 0x10000 by the sign of the
+// reference byte (b >= 128 -> high half): PRMT sign-replicate + 1.
+__device__ __forceinline__ uint32_t packed_inc(uint32_t Q, int j) {
+  return __byte_perm(Q, 0u, 0x4400u | ((8u + j) << 4) | (8u + j)) + 1u;
+}
+
+// A u16 field never wraps: each CTA round adds <= 32768 to the CTA's counters
+// and every field is < 0x8000 at a round boundary, so a field crossing
+// 0x7fff -> 0x8000 is seen by exactly one atomic (bit 15 of its field flips
+// 0 -> 1: ~old & new), whose thread moves 0x8000 votes to the u64 cell.
+__device__ __forceinline__ void packed_fixup(uint32_t addr, uint32_t x, uint32_t old, uint32_t inc,
+                                             unsigned long long* glcm, uint32_t L) {
+  if ((~old & (old + inc)) & 0x80008000u) {
+    red_smem(addr, 0u - (inc << 15));
+    atomicAdd(glcm + ((x >> 8) & 0xFFu) * L + (x & 0xFFu), 0x8000ull);
+  }
+}
+
+template <int STRAT>
+__device__ __forceinline__ void emit(uint32_t hb, uint32_t P, uint32_t Q, int j, uint32_t n,
+                                     unsigned long long* glcm, uint32_t L) {
+  const uint32_t x = pair_x(P, Q, j);
+  const uint32_t addr = vote_addr<STRAT>(hb, x);
+  if constexpr (STRAT == S_PACKED16) {
+    const uint32_t inc = packed_inc(Q, j) * n;
+    packed_fixup(addr, x, atom_smem(addr, inc), inc, glcm, L);
+  } else {
+    red_smem(addr, n);
+  }
+}
+
+// Votes the 16 pixel pairs of one item. Returns true when the run-length
+// shortcut fired (all 16 pairs identical: one vote of weight 16).
+template <int STRAT>
+__device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], const uint32_t (&Q)[4],
+                                       uint32_t mask, bool rle, unsigned long long* glcm, uint32_t L) {
   if (mask == 0xFFFFu) {
-    // run-length shortcut: a segment whose 16 pairs are identical (smooth
-    // inputs: 95-99.7% of neighbouring pairs repeat) casts ONE
-    // vote of weight 16 instead of 16 colliding atomics.
-    const uint32_t c0 = E[0] & 0xFFFFu;
-    const uint32_t bc = c0 | (c0 << 16);
-    const uint32_t diff = ((E[0] ^ bc) | (O[0] ^ bc)) | ((E[1] ^ bc) | (O[1] ^ bc)) |
-                          ((E[2] ^ bc) | (O[2] ^ bc)) | ((E[3] ^ bc) | (O[3] ^ bc));
-    if (diff == 0) {
-      emit<STRAT>(h, c0, 16u, glcm);
-      return;
+    if (rle) {
+      // smooth inputs (95-99.7% of neighbouring pairs repeat)
+      const uint32_t bp = __byte_perm(P[0], 0u, 0u), bq = __byte_perm(Q[0], 0u, 0u);
+      const uint32_t diff = (P[0] ^ bp) | (P[1] ^ bp) | (P[2] ^ bp) | (P[3] ^ bp) | (Q[0] ^ bq) |
+                            (Q[1] ^ bq) | (Q[2] ^ bq) | (Q[3] ^ bq);
+      if (diff == 0) {
+        emit<STRAT>(hb, P[0], Q[0], 0, 16u, glcm, L);
+        return true;
+      }
     }
+    if constexpr (STRAT == S_PACKED16) {
+      // 4 atomics (one word) back to back, then their spill checks
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      emit<STRAT>(h, E[i] & 0xFFFFu, 1u, glcm);
-      emit<STRAT>(h, O[i] & 0xFFFFu, 1u, glcm);
-      emit<STRAT>(h, E[i] >> 16, 1u, glcm);
-      emit<STRAT>(h, O[i] >> 16, 1u, glcm);
+      for (int i = 0; i < 4; ++i) {
+        uint32_t old[4], inc[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          inc[j] = packed_inc(Q[i], j);
+          old[j] = atom_smem(vote_addr<STRAT>(hb, pair_x(P[i], Q[i], j)), inc[j]);
+        }
+        uint32_t flag = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) flag |= ~old[j] & (old[j] + inc[j]);
+        if (flag & 0x80008000u) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t x = pair_x(P[i], Q[i], j);
+            packed_fixup(vote_addr<STRAT>(hb, x), x, old[j], inc[j], glcm, L);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) red_smem1(vote_addr<STRAT>(hb, pair_x(P[i], Q[i], j)));
     }
   } else if (mask) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (mask & (1u << (4 * i + 0))) emit<STRAT>(h, E[i] & 0xFFFFu, 1u, glcm);
-      if (mask & (1u << (4 * i + 1))) emit<STRAT>(h, O[i] & 0xFFFFu, 1u, glcm);
-      if (mask & (1u << (4 * i + 2))) emit<STRAT>(h, E[i] >> 16, 1u, glcm);
-      if (mask & (1u << (4 * i + 3))) emit<STRAT>(h, O[i] >> 16, 1u, glcm);
-    }
+    for (int k = 0; k < 16; ++k)
+      if (mask & (1u << k)) emit<STRAT>(hb, P[k >> 2], Q[k >> 2], k & 3, 1u, glcm, L);
   }
+  return false;
+}
+
+// Layout position (in counters) of real cell (ref b, anchor a).
+template <int STRAT>
+__device__ __forceinline__ uint32_t cell_pos(uint32_t b, uint32_t a) {
+  if constexpr (STRAT == S_COPIES32) return a + 32u * b;
+  else if constexpr (STRAT == S_COPIES8) return b + 64u * a;
+  else if constexpr (STRAT == S_COPY1) return a + 128u * b;
+  else return a + 256u * b;
 }
 
 __device__ __forceinline__ uint4 ldg16(const uint8_t* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }
 
+// ---------------------------------------------------------------------------
 // The three 16-byte loads of one item (anchor segment + the two aligned
 // segments that contain its reference bytes) and its valid-anchor mask.
 struct RawItem {
@@ -157,31 +257,34 @@ struct RawItem {
 // Issues the loads of item (row, j). Interior segments (0 < j < nch-1) need no
 // bounds logic: every reference byte of an interior segment lies inside the
 // row, so only the two edge segments of a row pay for masks.
+// Nothing here consumes a loaded value, so the loads stay in flight while the
+// caller votes the previous batch.
 template <int KSEL>
-__device__ __forceinline__ void issue_item(const VoteParams& p, const uint8_t* band, long long row, int j,
+__device__ __forceinline__ void issue_item(const VoteParams& p, const uint8_t* band, uint32_t row, uint32_t j,
                                            bool live, RawItem& it) {
-  it.a = it.c0 = it.c1 = make_uint4(0, 0, 0, 0);
+  // No zero-fill: bytes of a dead item or of an out-of-row reference segment
+  // only ever feed masked-off anchors (mask bit 0), so they are never voted.
   it.mask = 0;
   if (!live) return;
-  const int col0 = (p.ch0 + j) << 4;
+  const uint32_t col0 = (p.ch0 + j) << 4;
   const uint8_t* ap = band + (unsigned long long)row * p.pitch + col0;
   const uint8_t* rp = ap + p.ref_off;
   it.a = ldg16(ap);
-  if (j > 0 && j < p.nch - 1) {
+  if (j > 0 && j + 1 < (uint32_t)p.nch) {
     it.mask = 0xFFFFu;
-    it.c0 = ldg16(rp);
+    if (p.ref_off != 0) it.c0 = ldg16(rp);  // ref_off == 0: c0 is the anchor itself
     if constexpr (KSEL != 4) it.c1 = ldg16(rp + 16);
     return;
   }
-  const int lo = p.col_begin - col0;
-  const int hi = p.col_end - col0;
+  const int lo = p.col_begin - (int)col0;
+  const int hi = p.col_end - (int)col0;
   uint32_t m = 0xFFFFu;
   if (lo > 0) m &= 0xFFFFu << lo;
   if (hi < 16) m &= (1u << hi) - 1u;
   it.mask = m;
   const long long cs = (long long)col0 + p.qoff;
   const long long pitch = (long long)p.pitch;
-  if (cs >= 0 && cs < pitch) it.c0 = ldg16(rp);
+  if (p.ref_off != 0 && cs >= 0 && cs < pitch) it.c0 = ldg16(rp);
   if constexpr (KSEL != 4) {
     if (cs + 16 >= 0 && cs + 16 < pitch) it.c1 = ldg16(rp + 16);
   }
@@ -192,16 +295,18 @@ template <int KSEL>
 __device__ __forceinline__ void ref_words(const VoteParams& p, const RawItem& it, uint32_t (&A)[4],
                                           uint32_t (&R)[4]) {
   A[0] = it.a.x; A[1] = it.a.y; A[2] = it.a.z; A[3] = it.a.w;
+  const uint4 c0 = p.ref_off == 0 ? it.a : it.c0;
   if constexpr (KSEL == 4) {
-    R[0] = it.c0.x; R[1] = it.c0.y; R[2] = it.c0.z; R[3] = it.c0.w;
+    R[0] = c0.x; R[1] = c0.y; R[2] = c0.z; R[3] = c0.w;
   } else {
-    const uint32_t W[8] = {it.c0.x, it.c0.y, it.c0.z, it.c0.w, it.c1.x, it.c1.y, it.c1.z, it.c1.w};
+    const uint32_t W[8] = {c0.x, c0.y, c0.z, c0.w, it.c1.x, it.c1.y, it.c1.z, it.c1.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) R[i] = __funnelshift_r(W[i + KSEL], W[i + KSEL + 1], p.sbits);
   }
 }
 
-template <int QUANT, int STRAT>
+// Generic cell words for Scheme 1: u16 lanes cell = ref*L + anchor.
+template <int QUANT>
 __device__ __forceinline__ void cells_of(const VoteParams& p, const uint32_t (&A)[4],
                                          const uint32_t (&R)[4], uint32_t (&E)[4], uint32_t (&O)[4]) {
   const uint32_t L = (uint32_t)p.levels;
@@ -209,23 +314,34 @@ __device__ __forceinline__ void cells_of(const VoteParams& p, const uint32_t (&A
   for (int i = 0; i < 4; ++i) {
     const uint32_t a = quant4<QUANT>(A[i], p);
     const uint32_t b = quant4<QUANT>(R[i], p);
-    // u16 lanes: cell = ref*L + anchor (< 65536 for L <= 256, no lane carry)
     E[i] = (a & 0x00FF00FFu) + (b & 0x00FF00FFu) * L;
     O[i] = ((a >> 8) & 0x00FF00FFu) + ((b >> 8) & 0x00FF00FFu) * L;
   }
 }
 
+// q = n / d for n < 2^31 via a precomputed multiplier (d == 1: mul = 0).
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t shr) {
+  return mul ? (__umulhi(n, mul) >> shr) : n;
+}
+
 // ---------------------------------------------------------------------------
 // K1 + K2: fused quantise, vote, privatised merge.
-// Each thread walks items tid, tid+1024, ... of its CTA's contiguous item
-// range, with the NEXT item's loads in flight while the current one votes.
+//
+// Work distribution inside a CTA is dynamic: a warp takes batch tickets from
+// a shared counter, so fast warps take more batches and no warp idles at the
+// final barrier. PACKED16 groups tickets into rounds of 64 batches (2048
+// items = 32768 votes) separated by barriers: the u16 spill invariant.
 template <int QUANT, int STRAT, int KSEL>
 __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams p) {
   extern __shared__ __align__(16) uint32_t hist[];
+  __shared__ uint32_t s_ticket;
+  constexpr uint32_t kWarps = kThreads / 32;
+  constexpr uint32_t kRoundBatches = 64;
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
+  const uint32_t lane = tid & 31, warp = tid >> 5;
   const int band_idx = blockIdx.y;
   const uint8_t* band = p.img + (unsigned long long)band_idx * p.band_stride;
+  const uint32_t L = (uint32_t)p.levels;
   const int cells = p.levels * p.levels;
   unsigned long long* glcm = p.glcm + (size_t)band_idx * cells;
 
@@ -234,73 +350,102 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     const int n4 = p.hist_words >> 2;
     for (int i = tid; i < n4; i += kThreads) h4[i] = make_uint4(0, 0, 0, 0);
   }
+  if (tid == 0) s_ticket = kWarps;
 
-  uint32_t* h = hist;
-  if constexpr (STRAT == S_COPIES32) h += lane;
-  if constexpr (STRAT == S_COPIES8) h += (lane & 7);
+  uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(hist));
+  if constexpr (STRAT == S_COPIES32) hb += lane * 4u;
+  if constexpr (STRAT == S_COPIES8) hb += (lane & 7u) * 4u;
 
-  const long long start = (long long)blockIdx.x * p.items_per_cta;
-  long long end = start + p.items_per_cta;
-  if (end > p.items) end = p.items;
+  const long long start64 = (long long)blockIdx.x * p.items_per_cta;
+  const long long end64 = min(start64 + p.items_per_cta, p.items);
+  const uint32_t start = (uint32_t)start64;
+  const uint32_t n_items = end64 > start64 ? (uint32_t)(end64 - start64) : 0u;
+  const uint32_t n_batches = (n_items + 31) / 32;
 
-  long long row = 0;
-  int j = 0;
-  RawItem nxt;
-  if (start < end) {
-    const long long item = start + tid;
-    row = item / p.nch;
-    j = (int)(item - row * p.nch);
-    issue_item<KSEL>(p, band, row, j, item < end, nxt);
-  }
-  __syncthreads();  // histogram zeroed
+  auto issue_batch = [&](uint32_t t, RawItem& it) {
+    const uint32_t local = t * 32 + lane;
+    const uint32_t item = start + local;
+    const uint32_t row = fast_div(item, p.div_mul, p.div_shr);
+    const uint32_t j = item - row * (uint32_t)p.nch;
+    issue_item<KSEL>(p, band, row, j, t < n_batches && local < n_items, it);
+  };
+  auto grab = [&]() -> uint32_t {
+    uint32_t tn = 0;
+    if (lane == 0) tn = atomicAdd(&s_ticket, 1u);
+    return __shfl_sync(0xffffffffu, tn, 0);
+  };
 
-  int it = 0;
-  for (long long base = start; base < end; base += kThreads, ++it) {
-    const RawItem cur = nxt;
-    row += p.step_r;
-    j += p.step_j;
-    if (j >= p.nch) { j -= p.nch; ++row; }
-    issue_item<KSEL>(p, band, row, j, base + kThreads + tid < end, nxt);  // prefetch
-    uint32_t A[4], R[4], E[4], O[4];
-    ref_words<KSEL>(p, cur, A, R);
-    cells_of<QUANT, STRAT>(p, A, R, E, O);
-    vote16<STRAT>(h, E, O, cur.mask, glcm);
-    // PACKED16: <= 2 x 16384 votes per CTA between barriers (spill invariant)
+  // 3-slot register ring: batch k votes in place in its slot while batches
+  // k+1 and k+2 are in flight; the slot is refilled with batch k+3 after.
+  uint32_t t0 = warp, t1, t2;
+  RawItem n0, n1, n2;
+  issue_batch(t0, n0);
+  __syncthreads();  // histogram zeroed, ticket counter set
+  t1 = grab();
+  issue_batch(t1, n1);
+  t2 = grab();
+  issue_batch(t2, n2);
+
+  uint32_t barriers = 0;
+  bool rle = true;  // run-length check on; re-sampled every 8th batch when it stops paying
+  uint32_t nb = 0;
+  auto process = [&](const RawItem& cur, uint32_t t) {
     if constexpr (STRAT == S_PACKED16) {
-      if (it & 1) __syncthreads();
+      const uint32_t rnd = t / kRoundBatches;
+      while (barriers < rnd) {
+        __syncthreads();
+        ++barriers;
+      }
+    }
+    uint32_t A[4], R[4], P[4], Q[4];
+    ref_words<KSEL>(p, cur, A, R);
+    prep_words<QUANT, STRAT>(p, A, R, P, Q);
+    const bool check = rle || (nb & 7) == 0;
+    const bool hit = vote16<STRAT>(hb, P, Q, cur.mask, check, glcm, L);
+    if (check) rle = __popc(__ballot_sync(0xffffffffu, hit)) >= 4;  // >= 1/8 of the warp's segments
+    ++nb;
+  };
+  for (;;) {
+    if (t0 >= n_batches) break;
+    process(n0, t0);
+    t0 = grab();
+    issue_batch(t0, n0);
+    if (t1 >= n_batches) break;
+    process(n1, t1);
+    t1 = grab();
+    issue_batch(t1, n1);
+    if (t2 >= n_batches) break;
+    process(n2, t2);
+    t2 = grab();
+    issue_batch(t2, n2);
+  }
+  if constexpr (STRAT == S_PACKED16) {
+    const uint32_t rounds = (n_batches + kRoundBatches - 1) / kRoundBatches;
+    while (barriers + 1 < rounds) {
+      __syncthreads();
+      ++barriers;
     }
   }
   __syncthreads();
 
-  // K2 epilogue: merge the copies of each cell, then one global update per cell.
+  // K2 epilogue: merge the copies of each real cell (b, a), then one global
+  // update per cell (u64 atomics) or one plain store into this CTA's partial.
   uint32_t* part = p.partials
                        ? p.partials + ((size_t)band_idx * gridDim.x + blockIdx.x) * (size_t)cells
                        : nullptr;
-  if constexpr (STRAT == S_PACKED16) {
-    const int words = p.hist_words;
-    for (int w = tid; w < words; w += kThreads) {
-      const uint32_t v = hist[w];
-      const int c_lo = w, c_hi = w + 32768;
-      if (c_lo < cells) {
-        const uint32_t s = v & 0xFFFFu;
-        if (part) part[c_lo] = s;
-        else if (s) atomicAdd(glcm + c_lo, (unsigned long long)s);
-      }
-      if (c_hi < cells) {
-        const uint32_t s = v >> 16;
-        if (part) part[c_hi] = s;
-        else if (s) atomicAdd(glcm + c_hi, (unsigned long long)s);
-      }
-    }
-  } else {
-    constexpr int R = STRAT == S_COPIES32 ? 32 : (STRAT == S_COPIES8 ? 8 : 1);
-    for (int c = tid; c < cells; c += kThreads) {
-      uint32_t s = 0;
+  constexpr int RC = strat_copies(STRAT);
+  for (int c = tid; c < cells; c += kThreads) {
+    const uint32_t b = (uint32_t)c / L, a = (uint32_t)c - b * L;
+    const uint32_t pos = cell_pos<STRAT>(b, a);
+    uint32_t s = 0;
+    if constexpr (STRAT == S_PACKED16) {
+      s = (hist[pos & 0x7fffu] >> ((pos >> 11) & 16u)) & 0xFFFFu;
+    } else {
 #pragma unroll 8
-      for (int k = 0; k < R; ++k) s += hist[c * R + ((k + lane) & (R - 1))];
-      if (part) part[c] = s;
-      else if (s) atomicAdd(glcm + c, (unsigned long long)s);
+      for (int k = 0; k < RC; ++k) s += hist[pos * RC + ((k + lane) & (RC - 1))];
     }
+    if (part) part[c] = s;
+    else if (s) atomicAdd(glcm + c, (unsigned long long)s);
   }
 }
 
@@ -334,7 +479,7 @@ __global__ void glcm_vote_global_kernel(const VoteParams p) {
     issue_item<KSEL>(p, band, row, j, true, ri);
     uint32_t A[4], R[4], E[4], O[4];
     ref_words<KSEL>(p, ri, A, R);
-    cells_of<QUANT, S_COPY1>(p, A, R, E, O);
+    cells_of<QUANT>(p, A, R, E, O);
     const uint32_t m = ri.mask;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {

@@ -16,12 +16,13 @@ FEAT_TOL = 1e-10
 
 
 def _strategies_for(levels):
+    """Every vote layout that supports `levels` (tfg_kernels.cuh, enum Strat)."""
     s = [L.STRAT_PACKED16]
-    if levels * levels * 4 <= 227 * 1024:
+    if levels <= 128:
         s.append(L.STRAT_COPY1)
-    if levels * levels * 32 <= 227 * 1024:
+    if levels <= 64:
         s.append(L.STRAT_COPIES8)
-    if levels * levels * 128 <= 227 * 1024:
+    if levels <= 32:
         s.append(L.STRAT_COPIES32)
     return s
 

@@ -62,6 +62,32 @@ __global__ void __launch_bounds__(kT, 1) bench(unsigned long long* cycles, uint3
   if (acc == 0x12345678u) sink[0] = acc + s[lane];
 }
 
+// Distributed shared memory: a 2-CTA cluster, each CTA votes random words of
+// a 128 KB histogram half; `remote_pct` of the votes go to the peer CTA.
+template <int remote_pct>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT, 1) dsmem_bench(unsigned long long* cycles) {
+  extern __shared__ uint32_t s[];
+  for (int i = threadIdx.x; i < 32768; i += kT) s[i] = 0;
+  uint32_t rank, peer_base, local_base;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  local_base = static_cast<uint32_t>(__cvta_generic_to_shared(s));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer_base) : "r"(local_base), "r"(rank ^ 1));
+  asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  uint32_t h = threadIdx.x * 0x9E3779B9u + blockIdx.x * 0x85EBCA6Bu;
+  const unsigned long long t0 = clock64();
+#pragma unroll 8
+  for (int k = 0; k < kIters; ++k) {
+    h = h * 1664525u + 1013904223u;
+    const uint32_t r = h >> 9;
+    const bool remote = ((h >> 2) % 100u) < (uint32_t)remote_pct;
+    const uint32_t addr = (remote ? peer_base : local_base) + ((r & 32767u) << 2);
+    asm volatile("red.shared::cluster.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+  }
+  const unsigned long long t1 = clock64();
+  asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (threadIdx.x == 0) atomicMax(cycles, t1 - t0);
+}
+
 int main() {
   int dev = 0, sms = 0, clk = 0;
   cudaGetDevice(&dev);
@@ -93,6 +119,26 @@ int main() {
     const double ops = (double)sms * kT * kIters;
     printf("%s\"%s\": {\"ms\": %.4f, \"Gops_s\": %.1f, \"ops_per_clk_per_sm\": %.3f, \"sm_mhz_est\": %.0f}",
            m ? ", " : "", kNames[m], ms, ops / ms / 1e6, (double)kT * kIters / (double)c, c / (ms * 1e3));
+  }
+  using D = void (*)(unsigned long long*);
+  D ds[3] = {dsmem_bench<0>, dsmem_bench<50>, dsmem_bench<100>};
+  const char* dn[3] = {"dsmem_red_0pct_remote", "dsmem_red_50pct_remote", "dsmem_red_100pct_remote"};
+  for (int m = 0; m < 3; ++m) {
+    cudaFuncSetAttribute(ds[m], cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(cyc, 0, 8);
+      cudaEventRecord(a);
+      ds[m]<<<sms, kT, 131072>>>(cyc);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    unsigned long long c = 0;
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    const double ops = (double)sms * kT * kIters;
+    printf(", \"%s\": {\"ms\": %.4f, \"Gops_s\": %.1f, \"ops_per_clk_per_sm\": %.3f}", dn[m], ms, ops / ms / 1e6,
+           (double)kT * kIters / (double)c);
   }
   printf("}, \"err\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

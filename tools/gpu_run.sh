@@ -16,6 +16,8 @@ for s in $stages; do
       timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log ;;
     bench)
       timeout 900 python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err ;;
+    quick)
+      for L in 256 32; do timeout 300 python tools/profile_vote.py --levels $L --dts 1:0,1:45,2:90,4:135 --reps 5 --time > $OUT/timing_L$L.json 2>&1; done ;;
     timing)
       for L in 256 64 32 16 8; do timeout 300 python tools/profile_vote.py --levels $L --dts 1:0,1:45,2:90,4:135 --reps 5 --time > $OUT/timing_L$L.json 2>&1; done
       for S in 1 2 3 4; do timeout 300 python tools/profile_vote.py --levels 32 --strategy $S --dts 1:0 --reps 5 --time > $OUT/timing_L32_s$S.json 2>&1; done
@@ -23,6 +25,9 @@ for s in $stages; do
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_bench.json 2>&1
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:glcm_vote_kernel -c 2 -o $OUT/prof_c3 python tools/profile_vote.py --reps 1 > $OUT/ncu_full.log 2>&1 ;;
+    ncu32)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:glcm_vote_kernel -c 1 -o $OUT/prof_L32 python tools/profile_vote.py --levels 32 --kinds noise --reps 1 > $OUT/ncu_L32.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:glcm_vote_kernel -c 1 -o $OUT/prof_L256 python tools/profile_vote.py --levels 256 --kinds noise --reps 1 > $OUT/ncu_L256.log 2>&1 ;;
     benchref)
       timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err ;;
   esac
