@@ -289,6 +289,7 @@ VoteGeometry make_geometry(size_t width, size_t height, size_t pitch, size_t row
   const long d = distance;
   tfg::VoteParams& p = g.p;
   p.pitch = pitch;
+  p.buf_bytes = (unsigned long long)pitch * height;
   p.levels = levels;
   p.dr = (int)dr;
   const long qq = floor_div(dc, 16);

@@ -43,7 +43,8 @@ enum Strat : int {
   S_COPIES32 = 1,  // L <= 32:  32 u32 copies [a + 32b][lane]; P = 8a, Q = b, addr = 16x + 4 lane
   S_COPIES8 = 2,   // L <= 64:  8 u32 copies [b + 64a][lane%8]; P = 4b, Q = a, addr = 8x + 4 (lane%8)
   S_COPY1 = 3,     // L <= 128: 1 u32 copy [a + 128b]; P = 2a, Q = b, addr = 2x
-  S_PACKED16 = 4   // L <= 256: 1 copy of u16 counters, cell a + 256b in word (x & 0x7fff), half b >> 7
+  S_PACKED16 = 4   // L <= 256: 1 copy of u16 counters, cell a + 256b in word (x & 0x7fff), half b >> 7,
+                   //           spilled to the u64 cell every kSpill votes
 };
 
 __host__ __device__ constexpr int strat_scale(int s) {  // log2 of the P-byte scale
@@ -74,6 +75,7 @@ struct VoteParams {
   int hist_words;                   // shared-memory words
   unsigned long long* glcm;         // band b accumulator at glcm + b*L*L
   uint32_t* partials;               // null -> direct u64 atomics; else [band][grid][L*L]
+  unsigned long long buf_bytes;     // bytes of one band buffer (rows * pitch): prefetch clamp
 };
 
 // ---------------------------------------------------------------------------
@@ -123,10 +125,18 @@ __device__ __forceinline__ void prep_words(const VoteParams& p, const uint32_t (
   }
 }
 
+// PTX prmt, generic mode: selector nibble bits 2:0 pick a byte of {b, a},
+// bit 3 replicates that byte's sign (the __byte_perm intrinsic ignores bit 3).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
 // byte j of P in bits 0-7, byte j of Q in bits 8-15, bits 16-31 = sign of Q
 // byte 0 (zero: every Q byte of a non-packed layout is < 128).
 __device__ __forceinline__ uint32_t pair_x(uint32_t P, uint32_t Q, int j) {
-  return __byte_perm(P, Q, 0xCC00u | ((4u + j) << 4) | (uint32_t)j);
+  return prmt(P, Q, 0xCC00u | ((4u + j) << 4) | (uint32_t)j);
 }
 
 // ---------------------------------------------------------------------------
@@ -154,31 +164,44 @@ __device__ __forceinline__ uint32_t vote_addr(uint32_t hb, uint32_t x) {
 // PACKED16 increment for pixel j of word Q: 1 or 0x10000 by the sign of the
 // reference byte (b >= 128 -> high half): PRMT sign-replicate + 1.
 __device__ __forceinline__ uint32_t packed_inc(uint32_t Q, int j) {
-  return __byte_perm(Q, 0u, 0x4400u | ((8u + j) << 4) | (8u + j)) + 1u;
+  return prmt(Q, 0u, 0x4400u | ((8u + j) << 4) | (8u + j)) + 1u;
 }
 
-// A u16 field never wraps: each CTA round adds <= 32768 to the CTA's counters
-// and every field is < 0x8000 at a round boundary, so a field crossing
-// 0x7fff -> 0x8000 is seen by exactly one atomic (bit 15 of its field flips
-// 0 -> 1: ~old & new), whose thread moves 0x8000 votes to the u64 cell.
-__device__ __forceinline__ void packed_fixup(uint32_t addr, uint32_t x, uint32_t old, uint32_t inc,
+// PACKED16 spill rule (no barriers). A field spills kSpill = 2048 votes to
+// the u64 cell each time it crosses a multiple of kSpill: the crossing atomic
+// sees it exactly ((old ^ new) changes a bit >= 11 of its field) and its
+// thread subtracts kSpill. Every fix-up lowers the field across exactly one
+// multiple, so the crossings awaiting their fix-up on a field number exactly
+// floor(v / kSpill). A warp adds <= 512 to one field per item (32 lanes x 16)
+// and fences its fix-ups before its next item, so it holds <= 1 pending
+// crossing per field: v < (warps + 1) * kSpill = 25 * 2048 = 51200 < 2^16.
+constexpr uint32_t kSpill = 2048;
+static_assert((kThreads / 32 + 1) * kSpill + 512 <= 65535, "PACKED16 field bound");
+
+__device__ __forceinline__ bool packed_crossed(uint32_t old, uint32_t inc) {
+  return ((old ^ (old + inc)) & 0xF800F800u) != 0;
+}
+__device__ __forceinline__ bool packed_fixup(uint32_t addr, uint32_t x, uint32_t old, uint32_t inc,
                                              unsigned long long* glcm, uint32_t L) {
-  if ((~old & (old + inc)) & 0x80008000u) {
-    red_smem(addr, 0u - (inc << 15));
-    atomicAdd(glcm + ((x >> 8) & 0xFFu) * L + (x & 0xFFu), 0x8000ull);
+  if (packed_crossed(old, inc)) {
+    red_smem(addr, 0u - ((inc & 0xFFFFu) ? kSpill : (kSpill << 16)));
+    atomicAdd(glcm + ((x >> 8) & 0xFFu) * L + (x & 0xFFu), (unsigned long long)kSpill);
+    return true;
   }
+  return false;
 }
 
 template <int STRAT>
-__device__ __forceinline__ void emit(uint32_t hb, uint32_t P, uint32_t Q, int j, uint32_t n,
+__device__ __forceinline__ bool emit(uint32_t hb, uint32_t P, uint32_t Q, int j, uint32_t n,
                                      unsigned long long* glcm, uint32_t L) {
   const uint32_t x = pair_x(P, Q, j);
   const uint32_t addr = vote_addr<STRAT>(hb, x);
   if constexpr (STRAT == S_PACKED16) {
     const uint32_t inc = packed_inc(Q, j) * n;
-    packed_fixup(addr, x, atom_smem(addr, inc), inc, glcm, L);
+    return packed_fixup(addr, x, atom_smem(addr, inc), inc, glcm, L);
   } else {
     red_smem(addr, n);
+    return false;
   }
 }
 
@@ -186,7 +209,8 @@ __device__ __forceinline__ void emit(uint32_t hb, uint32_t P, uint32_t Q, int j,
 // shortcut fired (all 16 pairs identical: one vote of weight 16).
 template <int STRAT>
 __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], const uint32_t (&Q)[4],
-                                       uint32_t mask, bool rle, unsigned long long* glcm, uint32_t L) {
+                                       uint32_t mask, bool rle, unsigned long long* glcm, uint32_t L,
+                                       bool& fixed) {
   if (mask == 0xFFFFu) {
     if (rle) {
       // smooth inputs (95-99.7% of neighbouring pairs repeat)
@@ -194,7 +218,7 @@ __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], cons
       const uint32_t diff = (P[0] ^ bp) | (P[1] ^ bp) | (P[2] ^ bp) | (P[3] ^ bp) | (Q[0] ^ bq) |
                             (Q[1] ^ bq) | (Q[2] ^ bq) | (Q[3] ^ bq);
       if (diff == 0) {
-        emit<STRAT>(hb, P[0], Q[0], 0, 16u, glcm, L);
+        fixed |= emit<STRAT>(hb, P[0], Q[0], 0, 16u, glcm, L);
         return true;
       }
     }
@@ -210,12 +234,12 @@ __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], cons
         }
         uint32_t flag = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) flag |= ~old[j] & (old[j] + inc[j]);
-        if (flag & 0x80008000u) {
+        for (int j = 0; j < 4; ++j) flag |= old[j] ^ (old[j] + inc[j]);
+        if (flag & 0xF800F800u) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint32_t x = pair_x(P[i], Q[i], j);
-            packed_fixup(vote_addr<STRAT>(hb, x), x, old[j], inc[j], glcm, L);
+            fixed |= packed_fixup(vote_addr<STRAT>(hb, x), x, old[j], inc[j], glcm, L);
           }
         }
       }
@@ -228,10 +252,12 @@ __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], cons
   } else if (mask) {
 #pragma unroll
     for (int k = 0; k < 16; ++k)
-      if (mask & (1u << k)) emit<STRAT>(hb, P[k >> 2], Q[k >> 2], k & 3, 1u, glcm, L);
+      if (mask & (1u << k)) fixed |= emit<STRAT>(hb, P[k >> 2], Q[k >> 2], k & 3, 1u, glcm, L);
   }
   return false;
 }
+
+
 
 // Layout position (in counters) of real cell (ref b, anchor a).
 template <int STRAT>
@@ -244,6 +270,12 @@ __device__ __forceinline__ uint32_t cell_pos(uint32_t b, uint32_t a) {
 
 __device__ __forceinline__ uint4 ldg16(const uint8_t* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+// Bulk prefetch of [a, a+bytes) into L2 (cp.async.bulk.prefetch.L2, sm_90+):
+// one instruction moves a whole span of image rows towards the SMs.
+__device__ __forceinline__ void prefetch_l2(const void* a, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -329,14 +361,13 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t 
 //
 // Work distribution inside a CTA is dynamic: a warp takes batch tickets from
 // a shared counter, so fast warps take more batches and no warp idles at the
-// final barrier. PACKED16 groups tickets into rounds of 64 batches (2048
-// items = 32768 votes) separated by barriers: the u16 spill invariant.
+// final barrier. There is no barrier in the vote loop (PACKED16 included:
+// see kSpill).
 template <int QUANT, int STRAT, int KSEL>
 __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams p) {
   extern __shared__ __align__(16) uint32_t hist[];
   __shared__ uint32_t s_ticket;
   constexpr uint32_t kWarps = kThreads / 32;
-  constexpr uint32_t kRoundBatches = 64;
   const int tid = threadIdx.x;
   const uint32_t lane = tid & 31, warp = tid >> 5;
   const int band_idx = blockIdx.y;
@@ -369,9 +400,23 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     const uint32_t j = item - row * (uint32_t)p.nch;
     issue_item<KSEL>(p, band, row, j, t < n_batches && local < n_items, it);
   };
+  // Every 32nd ticket also pulls the reference bytes (the leading edge of the
+  // stream) of batches [t+96, t+128) into L2, ahead of the register ring.
   auto grab = [&]() -> uint32_t {
     uint32_t tn = 0;
-    if (lane == 0) tn = atomicAdd(&s_ticket, 1u);
+    if (lane == 0) {
+      tn = atomicAdd(&s_ticket, 1u);
+      if ((tn & 31u) == 0 && tn + 96 < n_batches) {
+        const uint32_t i0 = start + (tn + 96) * 32;
+        const uint32_t i1 = start + min(n_items, (tn + 128) * 32) - 1;
+        const uint32_t r0 = fast_div(i0, p.div_mul, p.div_shr), r1 = fast_div(i1, p.div_mul, p.div_shr);
+        long long a0 = (long long)r0 * (long long)p.pitch + ((p.ch0 + (i0 - r0 * (uint32_t)p.nch)) << 4) + p.ref_off;
+        long long a1 = (long long)r1 * (long long)p.pitch + ((p.ch0 + (i1 - r1 * (uint32_t)p.nch)) << 4) + p.ref_off + 32;
+        a0 = max(a0, 0ll);
+        a1 = min(a1, (long long)p.buf_bytes);
+        if (a1 > a0) prefetch_l2(band + a0, (uint32_t)min(a1 - a0, 1ll << 20) & ~15u);
+      }
+    }
     return __shfl_sync(0xffffffffu, tn, 0);
   };
 
@@ -386,23 +431,20 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   t2 = grab();
   issue_batch(t2, n2);
 
-  uint32_t barriers = 0;
   bool rle = true;  // run-length check on; re-sampled every 8th batch when it stops paying
   uint32_t nb = 0;
   auto process = [&](const RawItem& cur, uint32_t t) {
-    if constexpr (STRAT == S_PACKED16) {
-      const uint32_t rnd = t / kRoundBatches;
-      while (barriers < rnd) {
-        __syncthreads();
-        ++barriers;
-      }
-    }
     uint32_t A[4], R[4], P[4], Q[4];
     ref_words<KSEL>(p, cur, A, R);
     prep_words<QUANT, STRAT>(p, A, R, P, Q);
     const bool check = rle || (nb & 7) == 0;
-    const bool hit = vote16<STRAT>(hb, P, Q, cur.mask, check, glcm, L);
+    bool fixed = false;
+    const bool hit = vote16<STRAT>(hb, P, Q, cur.mask, check, glcm, L, fixed);
     if (check) rle = __popc(__ballot_sync(0xffffffffu, hit)) >= 4;  // >= 1/8 of the warp's segments
+    // PACKED16: this warp's fix-ups happen-before its next item's atomics
+    if constexpr (STRAT == S_PACKED16) {
+      if (__any_sync(0xffffffffu, fixed)) __syncwarp();
+    }
     ++nb;
   };
   for (;;) {
@@ -418,13 +460,6 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     process(n2, t2);
     t2 = grab();
     issue_batch(t2, n2);
-  }
-  if constexpr (STRAT == S_PACKED16) {
-    const uint32_t rounds = (n_batches + kRoundBatches - 1) / kRoundBatches;
-    while (barriers + 1 < rounds) {
-      __syncthreads();
-      ++barriers;
-    }
   }
   __syncthreads();
 
