@@ -199,6 +199,10 @@ VoteKernel pick_k(int ksel) {
     case 1: return tfg::glcm_vote_kernel<Q, S, 1>;
     case 2: return tfg::glcm_vote_kernel<Q, S, 2>;
     case 3: return tfg::glcm_vote_kernel<Q, S, 3>;
+    case 5: return tfg::glcm_vote_kernel<Q, S, 5>;
+    case 6: return tfg::glcm_vote_kernel<Q, S, 6>;
+    case 7: return tfg::glcm_vote_kernel<Q, S, 7>;
+    case 8: return tfg::glcm_vote_kernel<Q, S, 8>;
     default: return tfg::glcm_vote_kernel<Q, S, 4>;
   }
 }
@@ -221,7 +225,7 @@ VoteKernel pick_vote(int quant, int strat, int ksel) {
 }
 template <int Q>
 VoteKernel pick_g(int ksel) {
-  switch (ksel) {
+  switch (ksel >= 5 ? ksel - 5 : ksel) {  // Scheme 1 always loads c0
     case 0: return tfg::glcm_vote_global_kernel<Q, 0>;
     case 1: return tfg::glcm_vote_global_kernel<Q, 1>;
     case 2: return tfg::glcm_vote_global_kernel<Q, 2>;
@@ -296,6 +300,7 @@ VoteGeometry make_geometry(size_t width, size_t height, size_t pitch, size_t row
   p.qoff = (int)(qq * 16);
   const long rem = dc - qq * 16;  // 0..15
   g.ksel = rem == 0 ? 4 : (int)(rem >> 2);
+  if (g.ksel != 4 && dr == 0 && qq == 0) g.ksel += 5;  // theta = 0, d < 16: first ref segment = anchor
   p.sbits = (int)((rem & 3) * 8);
   p.ref_off = (long long)dr * (long long)pitch + p.qoff;
   p.col_begin = dc < 0 ? (int)d : 0;

@@ -205,6 +205,33 @@ __device__ __forceinline__ bool emit(uint32_t hb, uint32_t P, uint32_t Q, int j,
   }
 }
 
+// Rare paths live out of line so the hot loop fits the instruction cache.
+// Spill fix-ups of the 4 pixels of one word (PACKED16).
+__device__ __noinline__ bool packed_fix_word(uint32_t hb, uint32_t P, uint32_t Q, uint32_t o0, uint32_t o1,
+                                             uint32_t o2, uint32_t o3, unsigned long long* glcm, uint32_t L) {
+  const uint32_t old[4] = {o0, o1, o2, o3};
+  bool fixed = false;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t x = pair_x(P, Q, j);
+    fixed |= packed_fixup(vote_addr<S_PACKED16>(hb, x), x, old[j], packed_inc(Q, j), glcm, L);
+  }
+  return fixed;
+}
+
+// Edge segments of a row: only the anchors in `mask` vote.
+template <int STRAT>
+__device__ __noinline__ bool vote_masked(uint32_t hb, uint32_t P0, uint32_t P1, uint32_t P2, uint32_t P3,
+                                         uint32_t Q0, uint32_t Q1, uint32_t Q2, uint32_t Q3, uint32_t mask,
+                                         unsigned long long* glcm, uint32_t L) {
+  const uint32_t P[4] = {P0, P1, P2, P3}, Q[4] = {Q0, Q1, Q2, Q3};
+  bool fixed = false;
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (mask & (1u << k)) fixed |= emit<STRAT>(hb, P[k >> 2], Q[k >> 2], k & 3, 1u, glcm, L);
+  return fixed;
+}
+
 // Votes the 16 pixel pairs of one item. Returns true when the run-length
 // shortcut fired (all 16 pairs identical: one vote of weight 16).
 template <int STRAT>
@@ -235,13 +262,7 @@ __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], cons
         uint32_t flag = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) flag |= old[j] ^ (old[j] + inc[j]);
-        if (flag & 0xF800F800u) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t x = pair_x(P[i], Q[i], j);
-            fixed |= packed_fixup(vote_addr<STRAT>(hb, x), x, old[j], inc[j], glcm, L);
-          }
-        }
+        if (flag & 0xF800F800u) fixed |= packed_fix_word(hb, P[i], Q[i], old[0], old[1], old[2], old[3], glcm, L);
       }
     } else {
 #pragma unroll
@@ -250,9 +271,7 @@ __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], cons
         for (int j = 0; j < 4; ++j) red_smem1(vote_addr<STRAT>(hb, pair_x(P[i], Q[i], j)));
     }
   } else if (mask) {
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (mask & (1u << k)) fixed |= emit<STRAT>(hb, P[k >> 2], Q[k >> 2], k & 3, 1u, glcm, L);
+    fixed |= vote_masked<STRAT>(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], mask, glcm, L);
   }
   return false;
 }
@@ -286,6 +305,16 @@ struct RawItem {
   uint32_t mask;
 };
 
+// KSEL: how the 16 reference bytes sit in the two aligned segments c0:c1 —
+// bytes [4k+s, 4k+s+16) with k = KSEL (0..3, c0 loaded), KSEL == 4: c0 alone
+// (dcol % 16 == 0), k = KSEL-5 (5..8): same as k but c0 IS the anchor
+// segment (theta = 0, d < 16: one load fewer).
+template <int KSEL>
+__device__ __forceinline__ constexpr bool ksel_c0_is_anchor() { return KSEL >= 5; }
+template <int KSEL>
+__device__ __forceinline__ constexpr bool ksel_needs_c1() { return KSEL != 4; }
+
+
 // Issues the loads of item (row, j). Interior segments (0 < j < nch-1) need no
 // bounds logic: every reference byte of an interior segment lies inside the
 // row, so only the two edge segments of a row pay for masks.
@@ -299,13 +328,13 @@ __device__ __forceinline__ void issue_item(const VoteParams& p, const uint8_t* b
   it.mask = 0;
   if (!live) return;
   const uint32_t col0 = (p.ch0 + j) << 4;
-  const uint8_t* ap = band + (unsigned long long)row * p.pitch + col0;
+  const uint8_t* ap = band + (unsigned long long)row * (uint32_t)p.pitch + col0;
   const uint8_t* rp = ap + p.ref_off;
   it.a = ldg16(ap);
   if (j > 0 && j + 1 < (uint32_t)p.nch) {
     it.mask = 0xFFFFu;
-    if (p.ref_off != 0) it.c0 = ldg16(rp);  // ref_off == 0: c0 is the anchor itself
-    if constexpr (KSEL != 4) it.c1 = ldg16(rp + 16);
+    if constexpr (!ksel_c0_is_anchor<KSEL>()) it.c0 = ldg16(rp);
+    if constexpr (ksel_needs_c1<KSEL>()) it.c1 = ldg16(rp + 16);
     return;
   }
   const int lo = p.col_begin - (int)col0;
@@ -316,24 +345,27 @@ __device__ __forceinline__ void issue_item(const VoteParams& p, const uint8_t* b
   it.mask = m;
   const long long cs = (long long)col0 + p.qoff;
   const long long pitch = (long long)p.pitch;
-  if (p.ref_off != 0 && cs >= 0 && cs < pitch) it.c0 = ldg16(rp);
-  if constexpr (KSEL != 4) {
+  if constexpr (!ksel_c0_is_anchor<KSEL>()) {
+    if (cs >= 0 && cs < pitch) it.c0 = ldg16(rp);
+  }
+  if constexpr (ksel_needs_c1<KSEL>()) {
     if (cs + 16 >= 0 && cs + 16 < pitch) it.c1 = ldg16(rp + 16);
   }
 }
 
-// Reference bytes R[0..3] of an item: bytes [4k+s, 4k+s+16) of c0:c1.
+// Reference bytes R[0..3] of an item.
 template <int KSEL>
 __device__ __forceinline__ void ref_words(const VoteParams& p, const RawItem& it, uint32_t (&A)[4],
                                           uint32_t (&R)[4]) {
   A[0] = it.a.x; A[1] = it.a.y; A[2] = it.a.z; A[3] = it.a.w;
-  const uint4 c0 = p.ref_off == 0 ? it.a : it.c0;
+  const uint4 c0 = ksel_c0_is_anchor<KSEL>() ? it.a : it.c0;
   if constexpr (KSEL == 4) {
     R[0] = c0.x; R[1] = c0.y; R[2] = c0.z; R[3] = c0.w;
   } else {
+    constexpr int k = KSEL >= 5 ? KSEL - 5 : KSEL;
     const uint32_t W[8] = {c0.x, c0.y, c0.z, c0.w, it.c1.x, it.c1.y, it.c1.z, it.c1.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) R[i] = __funnelshift_r(W[i + KSEL], W[i + KSEL + 1], p.sbits);
+    for (int i = 0; i < 4; ++i) R[i] = __funnelshift_r(W[i + k], W[i + k + 1], p.sbits);
   }
 }
 
@@ -381,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     const int n4 = p.hist_words >> 2;
     for (int i = tid; i < n4; i += kThreads) h4[i] = make_uint4(0, 0, 0, 0);
   }
-  if (tid == 0) s_ticket = kWarps;
+  if (tid == 0) s_ticket = 3 * kWarps;
 
   uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(hist));
   if constexpr (STRAT == S_COPIES32) hb += lane * 4u;
@@ -393,43 +425,61 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   const uint32_t n_items = end64 > start64 ? (uint32_t)(end64 - start64) : 0u;
   const uint32_t n_batches = (n_items + 31) / 32;
 
+  // Batch t = items [start + 32t, start + 32t + 32). The common case — all 32
+  // live, in one row, none at the row's edges — is decided once per warp
+  // (uniform) and costs no per-lane predicates: lane address = base + 16 lane.
   auto issue_batch = [&](uint32_t t, RawItem& it) {
-    const uint32_t local = t * 32 + lane;
-    const uint32_t item = start + local;
-    const uint32_t row = fast_div(item, p.div_mul, p.div_shr);
-    const uint32_t j = item - row * (uint32_t)p.nch;
-    issue_item<KSEL>(p, band, row, j, t < n_batches && local < n_items, it);
+    const uint32_t item0 = start + t * 32;
+    const uint32_t row0 = fast_div(item0, p.div_mul, p.div_shr);
+    const uint32_t j0 = item0 - row0 * (uint32_t)p.nch;
+    if ((t + 1) * 32 <= n_items && j0 >= 1 && j0 + 32 < (uint32_t)p.nch) {
+      const uint8_t* ap = band + (unsigned long long)row0 * (uint32_t)p.pitch + ((p.ch0 + j0 + lane) << 4);
+      it.a = ldg16(ap);
+      if constexpr (!ksel_c0_is_anchor<KSEL>()) it.c0 = ldg16(ap + p.ref_off);
+      if constexpr (ksel_needs_c1<KSEL>()) it.c1 = ldg16(ap + p.ref_off + 16);
+      it.mask = 0xFFFFu;
+    } else {
+      const uint32_t local = t * 32 + lane;
+      const uint32_t item = start + local;
+      const uint32_t row = fast_div(item, p.div_mul, p.div_shr);
+      const uint32_t j = item - row * (uint32_t)p.nch;
+      issue_item<KSEL>(p, band, row, j, t < n_batches && local < n_items, it);
+    }
   };
   // Every 32nd ticket also pulls the reference bytes (the leading edge of the
   // stream) of batches [t+96, t+128) into L2, ahead of the register ring.
-  auto grab = [&]() -> uint32_t {
-    uint32_t tn = 0;
-    if (lane == 0) {
-      tn = atomicAdd(&s_ticket, 1u);
-      if ((tn & 31u) == 0 && tn + 96 < n_batches) {
-        const uint32_t i0 = start + (tn + 96) * 32;
-        const uint32_t i1 = start + min(n_items, (tn + 128) * 32) - 1;
-        const uint32_t r0 = fast_div(i0, p.div_mul, p.div_shr), r1 = fast_div(i1, p.div_mul, p.div_shr);
-        long long a0 = (long long)r0 * (long long)p.pitch + ((p.ch0 + (i0 - r0 * (uint32_t)p.nch)) << 4) + p.ref_off;
-        long long a1 = (long long)r1 * (long long)p.pitch + ((p.ch0 + (i1 - r1 * (uint32_t)p.nch)) << 4) + p.ref_off + 32;
-        a0 = max(a0, 0ll);
-        a1 = min(a1, (long long)p.buf_bytes);
-        if (a1 > a0) prefetch_l2(band + a0, (uint32_t)min(a1 - a0, 1ll << 20) & ~15u);
-      }
+  const uint32_t ticket_addr = static_cast<uint32_t>(__cvta_generic_to_shared(&s_ticket));
+  auto prefetch_ahead = [&](uint32_t tn) {
+    if ((tn & 31u) == 0 && tn + 96 < n_batches && lane == 0) {
+      const uint32_t i0 = start + (tn + 96) * 32;
+      const uint32_t i1 = start + min(n_items, (tn + 128) * 32) - 1;
+      const uint32_t r0 = fast_div(i0, p.div_mul, p.div_shr), r1 = fast_div(i1, p.div_mul, p.div_shr);
+      long long a0 = (long long)r0 * (long long)p.pitch + ((p.ch0 + (i0 - r0 * (uint32_t)p.nch)) << 4) + p.ref_off;
+      long long a1 = (long long)r1 * (long long)p.pitch + ((p.ch0 + (i1 - r1 * (uint32_t)p.nch)) << 4) + p.ref_off + 32;
+      a0 = max(a0, 0ll);
+      a1 = min(a1, (long long)p.buf_bytes);
+      if (a1 > a0) prefetch_l2(band + a0, (uint32_t)min(a1 - a0, 1ll << 20) & ~15u);
     }
-    return __shfl_sync(0xffffffffu, tn, 0);
+  };
+  // Tickets come in triples (one shared atomic per revolution of the ring).
+  auto grab3 = [&]() -> uint32_t {
+    uint32_t tn = 0;
+    if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 3;" : "=r"(tn) : "r"(ticket_addr) : "memory");
+    tn = __shfl_sync(0xffffffffu, tn, 0);
+    prefetch_ahead(tn);
+    prefetch_ahead(tn + 1);
+    prefetch_ahead(tn + 2);
+    return tn;
   };
 
   // 3-slot register ring: batch k votes in place in its slot while batches
   // k+1 and k+2 are in flight; the slot is refilled with batch k+3 after.
-  uint32_t t0 = warp, t1, t2;
+  uint32_t t0 = 3 * warp, t1 = 3 * warp + 1, t2 = 3 * warp + 2;
   RawItem n0, n1, n2;
   issue_batch(t0, n0);
-  __syncthreads();  // histogram zeroed, ticket counter set
-  t1 = grab();
   issue_batch(t1, n1);
-  t2 = grab();
   issue_batch(t2, n2);
+  __syncthreads();  // histogram zeroed, ticket counter set
 
   bool rle = true;  // run-length check on; re-sampled every 8th batch when it stops paying
   uint32_t nb = 0;
@@ -450,15 +500,16 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   for (;;) {
     if (t0 >= n_batches) break;
     process(n0, t0);
-    t0 = grab();
+    const uint32_t tn = grab3();
+    t0 = tn;
     issue_batch(t0, n0);
     if (t1 >= n_batches) break;
     process(n1, t1);
-    t1 = grab();
+    t1 = tn + 1;
     issue_batch(t1, n1);
     if (t2 >= n_batches) break;
     process(n2, t2);
-    t2 = grab();
+    t2 = tn + 2;
     issue_batch(t2, n2);
   }
   __syncthreads();
