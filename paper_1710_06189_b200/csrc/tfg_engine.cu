@@ -394,15 +394,28 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   per_band = std::max<long long>(per_band, 1);
   p.items_per_cta = (p.items + per_band - 1) / per_band;
   const bool use_partials = cells > 4096;
+  const bool packed_partials = use_partials && strat == tfg::S_PACKED16;
   if (use_partials) {
-    const size_t bytes = (size_t)per_band * n_bands * cells * 4;
+    const size_t per_cta = packed_partials ? words : cells;
+    const size_t bytes = (size_t)per_band * n_bands * per_cta * 4;
     p.partials = static_cast<uint32_t*>(ctx->partials.get(bytes));
   }
   dim3 grid((unsigned)per_band, (unsigned)n_bands);
   fn<<<grid, tfg::kThreads, smem, s>>>(p);
   ck(cudaGetLastError(), "glcm_vote_kernel launch");
   ctx->launches++;
-  if (use_partials) {
+  if (packed_partials) {
+    // split-K over the per-CTA partials: ~2 waves of 256-thread CTAs
+    const int xblocks = (int)((words / 4 + 255) / 256);
+    int splits = std::max(1, (int)std::min<long long>(per_band, (2LL * ctx->num_sms * 8) / std::max(xblocks * n_bands, 1)));
+    const int per_split = (int)((per_band + splits - 1) / splits);
+    splits = (int)((per_band + per_split - 1) / per_split);
+    dim3 rgrid((unsigned)xblocks, (unsigned)splits, (unsigned)n_bands);
+    tfg::glcm_reduce_packed_kernel<<<rgrid, 256, 0, s>>>(p.partials, (int)per_band, (int)words, levels, per_split,
+                                                          d_glcm);
+    ck(cudaGetLastError(), "glcm_reduce_packed_kernel launch");
+    ctx->launches++;
+  } else if (use_partials) {
     const long long total = (long long)cells * n_bands;
     const int rblocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx->num_sms * 8);
     tfg::glcm_reduce_partials_kernel<<<rblocks, 256, 0, s>>>(p.partials, (int)per_band, (int)cells,

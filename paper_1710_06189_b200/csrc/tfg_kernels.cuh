@@ -514,8 +514,19 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   }
   __syncthreads();
 
-  // K2 epilogue: merge the copies of each real cell (b, a), then one global
-  // update per cell (u64 atomics) or one plain store into this CTA's partial.
+  // K2 epilogue. PACKED16 with partials: the CTA's packed u16-pair words are
+  // stored as they are (coalesced 16-byte stores, half the bytes of u32 cells)
+  // and unpacked by glcm_reduce_packed_kernel. Otherwise: merge the copies of
+  // each real cell (b, a), then one u64 atomic per cell or one plain store
+  // into this CTA's u32 partial.
+  if constexpr (STRAT == S_PACKED16) {
+    if (p.partials) {
+      uint4* dst = reinterpret_cast<uint4*>(p.partials + ((size_t)band_idx * gridDim.x + blockIdx.x) * (size_t)p.hist_words);
+      const uint4* src = reinterpret_cast<const uint4*>(hist);
+      for (int i = tid; i < (p.hist_words >> 2); i += kThreads) dst[i] = src[i];
+      return;
+    }
+  }
   uint32_t* part = p.partials
                        ? p.partials + ((size_t)band_idx * gridDim.x + blockIdx.x) * (size_t)cells
                        : nullptr;
@@ -532,6 +543,38 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     }
     if (part) part[c] = s;
     else if (s) atomicAdd(glcm + c, (unsigned long long)s);
+  }
+}
+
+// Sum of per-CTA PACKED16 words into the u64 accumulator. Split-K: CTA
+// (x, y) sums partials [y*per, (y+1)*per) of words [4*(x*256+t), +4) with
+// 16-byte loads, then adds its 8 cell sums with u64 atomics (spread addresses).
+__global__ void __launch_bounds__(256) glcm_reduce_packed_kernel(const uint32_t* __restrict__ partials,
+                                                                  int nparts, int words, int levels,
+                                                                  int per_split,
+                                                                  unsigned long long* __restrict__ glcm) {
+  const int band = blockIdx.z;
+  const int w4 = blockIdx.x * blockDim.x + threadIdx.x;  // index of a 4-word group
+  if (w4 * 4 >= words) return;
+  const int g0 = blockIdx.y * per_split, g1 = min(nparts, g0 + per_split);
+  const uint4* src = reinterpret_cast<const uint4*>(partials + (size_t)band * nparts * words) + w4;
+  const size_t stride4 = (size_t)words / 4;
+  uint32_t lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+#pragma unroll 4
+  for (int g = g0; g < g1; ++g) {
+    const uint4 v = __ldg(src + g * stride4);
+    lo[0] += v.x & 0xFFFFu; hi[0] += v.x >> 16;
+    lo[1] += v.y & 0xFFFFu; hi[1] += v.y >> 16;
+    lo[2] += v.z & 0xFFFFu; hi[2] += v.z >> 16;
+    lo[3] += v.w & 0xFFFFu; hi[3] += v.w >> 16;
+  }
+  unsigned long long* out = glcm + (size_t)band * levels * levels;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t x = (uint32_t)(w4 * 4 + k);  // cell a + 256 b, b < 128
+    const uint32_t a = x & 0xFFu, b = x >> 8;
+    if (lo[k]) atomicAdd(out + b * levels + a, (unsigned long long)lo[k]);
+    if (hi[k]) atomicAdd(out + (b + 128) * levels + a, (unsigned long long)hi[k]);
   }
 }
 
