@@ -90,6 +90,8 @@ void tfg_ctx_destroy(tfg_ctx* ctx);
 const char* tfg_last_error(void);
 size_t tfg_last_error_chunk(void);
 int tfg_abi_version(void);
+/* where `p` lives: 0 pageable host, 1 pinned host, 2 device, 3 managed */
+int tfg_memory_kind(const void* p);
 /* number of engine kernels this context has launched (evidence counter) */
 uint64_t tfg_launch_count(tfg_ctx* ctx);
 
@@ -142,6 +144,20 @@ int tfg_glcm_chunked(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels
                      const int* distances, const int* angles_deg, int n_dt, size_t chunk_count,
                      tfg_fetch_fn fetch, void* user, unsigned flags, uint64_t* counts_out,
                      double* probs_out, double* feats_out);
+
+/*
+ * Privatised sub-GLCMs with the reference's exact routing (compute_subglcms,
+ * R/include/texforge/parallel.hpp:160-225; per_copy_hottest of
+ * compute_glcm_privatized, parallel.hpp:240-254): `group_count` groups own
+ * stripe_rows(height, group_count) (parallel.hpp:76-89); stripe pixel k votes
+ * into copy ((k - stripe_begin*width) mod group_size) mod copies.
+ * group_count must already be resolved by the caller (1 <= group_count <= height).
+ * subs_out: group_count*copies*L*L u32 (group-major) or NULL; counts_out: L*L
+ * u64 or NULL; per_copy_hottest_out: group_count*copies u64 or NULL.
+ */
+int tfg_subglcms(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, int pixel_levels, int levels,
+                 int distance, int angle_deg, unsigned group_size, unsigned copies, size_t group_count,
+                 unsigned flags, uint32_t* subs_out, uint64_t* counts_out, uint64_t* per_copy_hottest_out);
 
 /* post-processing on the device (host in/out) */
 int tfg_symmetrize(tfg_ctx* ctx, const uint64_t* counts, int levels, uint64_t* out);

@@ -51,6 +51,7 @@ SIGNATURES = [
     ("tfg_last_error", C.c_char_p, []),
     ("tfg_last_error_chunk", C.c_size_t, []),
     ("tfg_abi_version", C.c_int, []),
+    ("tfg_memory_kind", C.c_int, [C.c_void_p]),
     ("tfg_launch_count", C.c_uint64, [C.c_void_p]),
     ("tfg_neighbor_offset", C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_long), C.POINTER(C.c_long)]),
     ("tfg_valid_pair_count", C.c_int, [_sz, _sz, C.c_int, C.c_int, _u64p]),
@@ -65,6 +66,8 @@ SIGNATURES = [
                                  _ip, C.c_int, C.c_uint, _u64p, _dp, _dp]),
     ("tfg_glcm_chunked", C.c_int, [C.c_void_p, _sz, _sz, C.c_int, C.c_int, _ip, _ip, C.c_int, _sz, FETCH_FN,
                                    C.c_void_p, C.c_uint, _u64p, _dp, _dp]),
+    ("tfg_subglcms", C.c_int, [C.c_void_p, C.c_void_p, _sz, _sz, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint,
+                               C.c_uint, _sz, C.c_uint, C.POINTER(C.c_uint32), _u64p, _u64p]),
     ("tfg_symmetrize", C.c_int, [C.c_void_p, _u64p, C.c_int, _u64p]),
     ("tfg_normalize", C.c_int, [C.c_void_p, _u64p, C.c_int, _dp]),
     ("tfg_features", C.c_int, [C.c_void_p, _dp, C.c_int, _dp]),

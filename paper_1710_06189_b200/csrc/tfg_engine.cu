@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/texforge_cuda.h"
@@ -514,6 +515,38 @@ void check_async_flag(tfg_ctx* ctx, cudaStream_t s) {
   }
 }
 
+// 0 pageable host, 1 pinned host, 2 device, 3 managed (cudaPointerGetAttributes).
+int host_memory_kind(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  switch (a.type) {
+    case cudaMemoryTypeHost: return 1;
+    case cudaMemoryTypeDevice: return 2;
+    case cudaMemoryTypeManaged: return 3;
+    default: return 0;
+  }
+}
+
+// Host copy split over up to 8 threads (pageable -> pinned staging).
+void parallel_memcpy(uint8_t* dst, const uint8_t* src, size_t n) {
+  const size_t kMinPerThread = 4u << 20;
+  const size_t nt = std::min<size_t>(8, std::max<size_t>(1, n / kMinPerThread));
+  if (nt <= 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const size_t per = (n + nt - 1) / nt;
+  for (size_t t = 0; t < nt; ++t) {
+    const size_t b = t * per, e = std::min(n, b + per);
+    if (b < e) pool.emplace_back([=] { std::memcpy(dst + b, src + b, e - b); });
+  }
+  for (auto& th : pool) th.join();
+}
+
 size_t auto_chunks(size_t width, size_t height, int max_d) {
   const size_t bytes = width * height;
   const size_t target = 32u << 20;  // ~32 MiB per chunk
@@ -590,6 +623,7 @@ void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, i
 extern "C" {
 
 int tfg_abi_version(void) { return TFG_ABI_VERSION; }
+int tfg_memory_kind(const void* p) { return host_memory_kind(p); }
 const char* tfg_last_error(void) { return g_error.c_str(); }
 size_t tfg_last_error_chunk(void) { return g_error_chunk; }
 uint64_t tfg_launch_count(tfg_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
@@ -775,10 +809,23 @@ int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height,
       for (int i = 0; i < n_dt; ++i) dmax = std::max(dmax, distances[i]);
       const size_t k = auto_chunks(width, height, dmax);
       // per-(d,theta) accumulators are contiguous: d_acc + t*cells
+      if (pitch != width) fail(TFG_INVALID_ARGUMENT, "glcm: host images must be dense (pitch == width)");
+      // Pinned caller memory is DMA'd in place. Pageable memory would make
+      // every cudaMemcpyAsync a synchronous bounce-buffer copy, so its rows are
+      // first copied (by several host threads) into the pinned ring slot.
+      const bool pageable = host_memory_kind(px) == 0;
+      if (pageable) {
+        const std::vector<uint64_t> sp = chunk_specs(width, height, distances, angles_deg, n_dt, k);
+        size_t max_rows = 0;
+        for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, sp[3 * i + 2] - sp[3 * i]);
+        for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->hslot[sl].get(max_rows * width + 64);
+      }
       run_pipeline(ctx, width, height, pixel_levels, levels, distances, angles_deg, n_dt, k, flags, d_acc,
-                   [&](size_t, size_t start, size_t, size_t, int) -> const uint8_t* {
-                     if (pitch != width) fail(TFG_INVALID_ARGUMENT, "glcm: host images must be dense (pitch == width)");
-                     return px + start * width;
+                   [&](size_t, size_t start, size_t, size_t buf_end, int sl) -> const uint8_t* {
+                     if (!pageable) return px + start * width;
+                     uint8_t* dst = static_cast<uint8_t*>(ctx->hslot[sl].p);
+                     parallel_memcpy(dst, px + start * width, (buf_end - start) * width);
+                     return dst;
                    });
       if (pixel_levels == levels) check_async_flag(ctx, s);
       finish(ctx, d_acc, (int)n_out, levels, flags, counts_out, probs_out, feats_out, s);
@@ -871,6 +918,98 @@ int tfg_glcm_chunked(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels
     }
     if (pixel_levels == levels) check_async_flag(ctx, s);
     finish(ctx, d_acc, n_dt, levels, flags, counts_out, probs_out, feats_out, s);
+  });
+}
+
+int tfg_subglcms(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, int pixel_levels, int levels,
+                 int distance, int angle_deg, unsigned group_size, unsigned copies, size_t group_count,
+                 unsigned flags, uint32_t* subs_out, uint64_t* counts_out, uint64_t* per_copy_hottest_out) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded([&] {
+    check_levels(levels, "glcm");
+    check_pixel_levels(pixel_levels, levels);
+    if (width == 0 || height == 0) fail(TFG_INVALID_ARGUMENT, "QuantizedImage: dimensions must be positive");
+    check_angle(angle_deg);
+    check_geometry(width, height, distance);
+    if (copies < 1) fail(TFG_INVALID_ARGUMENT, "privatized: plan.copies must be >= 1");
+    if (group_size == 0) group_size = 512;
+    if (group_count < 1 || group_count > height)
+      fail(TFG_INVALID_ARGUMENT, "subglcms: group count must be in [1, height]");
+    if (!px) fail(TFG_INVALID_ARGUMENT, "glcm: null pixels");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = ctx->exec;
+    const size_t cells = (size_t)levels * levels;
+    const size_t n_subs = group_count * copies;
+    // stage the raster (host or device) into an aligned pitched buffer
+    const size_t dpitch = round16(width);
+    uint8_t* d_img = static_cast<uint8_t*>(ctx->img.get(dpitch * height + 64));
+    const bool dev = (flags & TFG_INPUT_DEVICE) != 0;
+    ck(cudaMemcpy2DAsync(d_img, dpitch, px, width, width, height,
+                         dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s),
+       "stage image");
+    if (pixel_levels == levels) launch_validate(ctx, d_img, width, height, dpitch, 0, 1, levels, ctx->d_err, s);
+    // work items: stripe_rows(height, group_count) (parallel.hpp:76-89), cut into <= 64-row pieces
+    std::vector<tfg::SubWork> work;
+    const size_t base = height / group_count, extra = height % group_count;
+    size_t row = 0;
+    for (size_t g = 0; g < group_count; ++g) {
+      const size_t end = row + base + (g < extra ? 1 : 0);
+      for (size_t r = row; r < end; r += 64)
+        work.push_back({(uint32_t)g, (uint32_t)r, (uint32_t)std::min(end, r + 64), (uint32_t)row});
+      row = end;
+    }
+    const size_t sub_bytes = n_subs * cells * 4;
+    char* scratch = static_cast<char*>(ctx->tmp.get(sub_bytes + work.size() * sizeof(tfg::SubWork) +
+                                                         n_subs * 8 + 256));
+    uint32_t* d_subs = reinterpret_cast<uint32_t*>(scratch);
+    auto* d_work = reinterpret_cast<tfg::SubWork*>(scratch + ((sub_bytes + 15) & ~size_t(15)));
+    auto* d_max = reinterpret_cast<unsigned long long*>(
+        scratch + ((sub_bytes + 15) & ~size_t(15)) + ((work.size() * sizeof(tfg::SubWork) + 15) & ~size_t(15)));
+    ck(cudaMemsetAsync(d_subs, 0, sub_bytes, s), "memset");
+    ck(cudaMemcpyAsync(d_work, work.data(), work.size() * sizeof(tfg::SubWork), cudaMemcpyHostToDevice, s),
+       "H2D work");
+    long dr, dc;
+    offset_of(distance, angle_deg, &dr, &dc);
+    tfg::SubParams sp{};
+    sp.img = d_img;
+    sp.pitch = dpitch;
+    sp.width = (int)width;
+    sp.height = (int)height;
+    sp.levels = levels;
+    sp.pixel_levels = pixel_levels;
+    sp.dr = (int)dr;
+    sp.dc = (int)dc;
+    sp.d = distance;
+    sp.group_size = group_size;
+    sp.copies = copies;
+    sp.work = d_work;
+    sp.subs = d_subs;
+    const size_t smem = copies * cells * 4;
+    sp.use_smem = smem <= 96 * 1024;
+    if (sp.use_smem && smem > 48 * 1024)
+      ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(tfg::glcm_subglcm_kernel),
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+         "cudaFuncSetAttribute");
+    tfg::glcm_subglcm_kernel<<<(unsigned)work.size(), 256, sp.use_smem ? smem : 0, s>>>(sp);
+    ck(cudaGetLastError(), "glcm_subglcm_kernel launch");
+    ctx->launches++;
+    if (per_copy_hottest_out) {
+      tfg::subglcm_max_kernel<<<(unsigned)n_subs, 256, 0, s>>>(d_subs, (int)cells, d_max);
+      ck(cudaGetLastError(), "subglcm_max_kernel launch");
+      ctx->launches++;
+      ck(cudaMemcpyAsync(per_copy_hottest_out, d_max, n_subs * 8, cudaMemcpyDeviceToHost, s), "D2H max");
+    }
+    if (subs_out) ck(cudaMemcpyAsync(subs_out, d_subs, sub_bytes, cudaMemcpyDeviceToHost, s), "D2H subs");
+    if (counts_out) {
+      auto* d_acc = static_cast<unsigned long long*>(ctx->acc.get(cells * 8));
+      ck(cudaMemsetAsync(d_acc, 0, cells * 8, s), "memset");
+      launch_vote(ctx, d_img, width, height, dpitch, 0, 1, height, pixel_levels, levels, distance, angle_deg,
+                  flags & ~TFG_INPUT_DEVICE, d_acc, s);
+      ck(cudaMemcpyAsync(counts_out, d_acc, cells * 8, cudaMemcpyDeviceToHost, s), "D2H counts");
+    }
+    ck(cudaStreamSynchronize(s), "stream sync");
+    if (pixel_levels == levels) check_async_flag(ctx, s);
   });
 }
 

@@ -620,6 +620,90 @@ __global__ void glcm_vote_global_kernel(const VoteParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Sub-GLCM export (compute_subglcms, parallel.hpp:160-225): the reference's
+// exact privatised layout — groups own contiguous row stripes, stripe pixel k
+// maps to lane (k - stripe_begin*width) mod group_size, and lane i votes into
+// copy (i mod R). One CTA per work item (a row range inside one stripe);
+// the R copies of the stripe live in shared memory when they fit, else the
+// votes go straight to the global u32 sub-GLCMs. Diagnostic/drop-in path, not
+// the throughput path (that is glcm_vote_kernel).
+struct SubWork {
+  uint32_t group, row0, row1, stripe_begin;
+};
+
+struct SubParams {
+  const uint8_t* img;
+  unsigned long long pitch;
+  int width, height, levels, pixel_levels;
+  int dr, dc, d;
+  uint32_t group_size, copies;
+  const SubWork* work;
+  uint32_t* subs;  // [group][copy][L*L]
+  int use_smem;
+};
+
+__global__ void __launch_bounds__(256) glcm_subglcm_kernel(const SubParams p) {
+  extern __shared__ uint32_t sh[];
+  const SubWork w = p.work[blockIdx.x];
+  const uint32_t cells = (uint32_t)p.levels * p.levels;
+  const uint32_t words = cells * p.copies;
+  if (p.use_smem) {
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+  }
+  uint32_t* gsub = p.subs + (size_t)w.group * words;
+  const int col_begin = p.dc < 0 ? p.d : 0;
+  const int col_end = p.dc > 0 ? p.width - p.d : p.width;
+  const int row_limit = p.height - p.dr;
+  const uint32_t row1 = min(w.row1, (uint32_t)max(row_limit, 0));
+  const uint32_t ncols = col_end > col_begin ? (uint32_t)(col_end - col_begin) : 0u;
+  const uint32_t L = (uint32_t)p.levels;
+  const bool quant = p.pixel_levels != p.levels;
+  if (w.row0 < row1 && ncols) {
+    const unsigned long long n = (unsigned long long)(row1 - w.row0) * ncols;
+    for (unsigned long long i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t r = w.row0 + (uint32_t)(i / ncols);
+      const uint32_t c = col_begin + (uint32_t)(i % ncols);
+      uint32_t a = p.img[(unsigned long long)r * p.pitch + c];
+      uint32_t b = p.img[(unsigned long long)(r + p.dr) * p.pitch + (c + p.dc)];
+      if (quant) {
+        a = (a * L) >> 8;
+        b = (b * L) >> 8;
+      }
+      const unsigned long long k = (unsigned long long)(r - w.stripe_begin) * (unsigned)p.width + c;
+      const uint32_t copy = (uint32_t)(k % p.group_size) % p.copies;
+      const uint32_t pos = copy * cells + b * L + a;
+      if (p.use_smem) atomicAdd(sh + pos, 1u);
+      else atomicAdd(gsub + pos, 1u);
+    }
+  }
+  if (p.use_smem) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
+      if (sh[i]) atomicAdd(gsub + i, sh[i]);
+  }
+}
+
+// Hottest cell of each sub-GLCM (ContentionStats::per_copy_hottest,
+// parallel.hpp:247-252); one CTA per sub-GLCM.
+__global__ void __launch_bounds__(256) subglcm_max_kernel(const uint32_t* __restrict__ subs, int cells,
+                                                          unsigned long long* __restrict__ out) {
+  __shared__ uint32_t s[8];
+  const uint32_t* g = subs + (size_t)blockIdx.x * cells;
+  uint32_t m = 0;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) m = max(m, g[c]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = max(m, s[i]);
+    m = max(m, s[0]);
+    out[blockIdx.x] = m;
+  }
+}
+
 // Validation of an already-quantised raster (QuantizedImage ctor, image.hpp:46-48).
 __global__ void validate_levels_kernel(const uint8_t* img, unsigned long long pitch, int width,
                                        long long rows, unsigned long long band_stride, int levels,

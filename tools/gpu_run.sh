@@ -28,6 +28,10 @@ for s in $stages; do
     ncu32)
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:glcm_vote_kernel -c 1 -o $OUT/prof_L32 python tools/profile_vote.py --levels 32 --kinds noise --reps 1 > $OUT/ncu_L32.log 2>&1
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:glcm_vote_kernel -c 1 -o $OUT/prof_L256 python tools/profile_vote.py --levels 256 --kinds noise --reps 1 > $OUT/ncu_L256.log 2>&1 ;;
+    cpp)
+      for b in dropin_tests refsuite_unit refsuite_accept; do timeout 900 tests/cpp/_build/$b > $OUT/cpp_$b.log 2>&1; echo "rc=$?" >> $OUT/cpp_$b.log; done ;;
+    e2e)
+      timeout 600 python tools/e2e_diag.py > $OUT/e2e_diag.json 2>&1 ;;
     benchref)
       timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err ;;
   esac
