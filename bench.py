@@ -1,19 +1,30 @@
 """Benchmark of the B200 GLCM engine (contract in DESIGN.md §6).
 
-Metric (BASELINE.json): GLCM Gpixel-pairs/s per (d, theta).
-Default workload = BASELINE config 3: 16384x16384, L=256, d in {1,2,4} x four
-theta, on BOTH the uniform-noise and the smooth-gradient input (the collision
-worst case). One step = the 24 GLCMs (2 images x 12 (d, theta)), each a
-separate single-(d, theta) engine launch over the device-resident image.
-Each input (256 MiB) is larger than L2 (126 MB), so no L2 flush is needed.
+Metric (BASELINE.json): GLCM Gpixel-pairs/s per (d, theta) = valid pixel
+pairs voted per second, whole job, summed over every (image, d, theta) GLCM.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload c3|c2|c4]
+Workloads (BASELINE.json configs; --workload, default c3):
+  c3  16384^2 per GPU, L=256, d in {1,2,4} x 4 theta, uniform-noise AND
+      smooth-gradient (the collision worst case): 24 GLCMs per step, one
+      engine launch each, image device-resident. N>1: the image is
+      (N*16384) x 16384, row-partitioned (partition(), pipeline.hpp:48-73):
+      each GPU owns 16384 rows + a 4-row halo received from its neighbour,
+      votes its owned anchors, and the 24 partial GLCMs are summed with ONE
+      NCCL reduce per step inside the timed region (weak scaling).
+  c5  65536^2 (4 GiB), L=64, d=1, 4 theta, noise, row-partitioned over N
+      GPUs with d-row halos + one NCCL reduce per step (strong scaling).
+  c4  256 bands of 2048^2, L=32, d=1, 4 theta, bands sharded over N GPUs,
+      one launch per theta for all of a GPU's bands, no collective (strong).
+  c2  4096^2, L=16 and 32, d=1, 4 theta, noise+smooth (replicas for N>1).
+  c1  512^2, L=8, d=1, 0 deg (the reference's CPU case; replicas).
 
-N>1 (under torchrun): every rank runs the same per-GPU workload on its own
-B200 (weak scaling: independent images, no data-path collective); time = max
-over ranks. --impl reference times the reference's own CPU path
-(oracle/_ref/libtexforge_ref.so = the unmodified reference headers,
-compute_glcm_privatized on all host threads) on the same workload, rank 0 only.
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload c3]
+
+Every input is larger than L2 (126 MB) except c1/c2/c4-per-band, where the
+L2 is flushed between timed steps (config.l2 says which). --impl reference
+times the reference's own CPU path (oracle/_ref/libtexforge_ref.so = the
+UNMODIFIED reference headers, compute_glcm_privatized on all host threads)
+on a bounded sample of the same workload, rank 0 only.
 """
 from __future__ import annotations
 
@@ -35,13 +46,21 @@ sys.path.insert(0, ROOT)
 METRIC = "GLCM Gpixel-pairs/s per (d,theta)"
 UNIT = "Gpairs/s"
 ANGLES = (0, 45, 90, 135)
+L2_BYTES = 126 * 1024 * 1024
 
+# name: width, rows per GPU block (None: whole image of `height` rows split over N),
+#       height, levels list, distances, kinds, layout, bands
 WORKLOADS = {
-    # name: (size, levels, distances, kinds, n_bands)
-    "c3": (16384, 256, (1, 2, 4), ("noise", "smooth"), 1),
-    "c2": (4096, 32, (1,), ("noise", "smooth"), 1),
-    "c4": (2048, 32, (1,), ("noise",), 32),
+    "c3": dict(width=16384, block_rows=16384, levels=(256,), ds=(1, 2, 4), kinds=("noise", "smooth"),
+               layout="rows-weak", bands=1),
+    "c5": dict(width=65536, height=65536, levels=(64,), ds=(1,), kinds=("noise",), layout="rows-strong", bands=1),
+    "c4": dict(width=2048, height=2048, levels=(32,), ds=(1,), kinds=("noise",), layout="bands", bands=256),
+    "c2": dict(width=4096, height=4096, levels=(16, 32), ds=(1,), kinds=("noise", "smooth"), layout="replica",
+               bands=1),
+    "c1": dict(width=512, height=512, levels=(8,), ds=(1,), kinds=("noise",), layout="replica", bands=1,
+               angles=(0,)),
 }
+GEN_BLOCK = 1024  # rows per generator block of the strong-scaling images (content independent of N)
 
 
 def log(*a):
@@ -56,28 +75,22 @@ def valid_pairs(w, h, d, a):
     return (h - d) * (w - d)
 
 
-def make_images(tf, n, kinds, n_bands, rank):
-    imgs = {}
-    for kind in kinds:
-        if n_bands == 1:
-            gen = tf.synth_noise if kind == "noise" else tf.synth_smooth
-            imgs[kind] = gen(n, n, 1).pixels
-        else:
-            imgs[kind] = np.concatenate([tf.synth_noise(n, n, b + 1 + rank * n_bands).pixels
-                                         for b in range(n_bands)])
-    return imgs
+def fnv1a64(counts: np.ndarray) -> str:
+    h = 0xcbf29ce484222325
+    for b in np.ascontiguousarray(counts, dtype="<u8").tobytes():
+        h = ((h ^ b) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return "%016x" % h
 
 
 class ClockSampler:
     """SM clock + throttle reasons sampled DURING the timed region (NVML every
     ~2 ms; nvidia-smi as fallback)."""
-    # nvmlClocksEventReason* bits
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device):
         self.device = device
-        self.samples = []  # (sm_mhz, reasons_mask)
+        self.samples = []
         self.sm_max = None
         self._stop = threading.Event()
         self._t = None
@@ -130,76 +143,175 @@ class ClockSampler:
 
 
 def hbm_peak():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
 def committed_traffic(workload):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             return json.load(f).get(workload)
     except Exception:
         return None
 
 
+# --------------------------------------------------------------------------- inputs
+def gen_rows(tf, kind, width, row0, rows, block_rows, seed0):
+    """Rows [row0, row0+rows) of an image made of generator blocks of
+    `block_rows` rows, block b = synth_<kind>(width, block_rows, seed0 + b).
+    The content does not depend on how the rows are later partitioned."""
+    gen = tf.synth_noise if kind == "noise" else tf.synth_smooth
+    out = np.empty(rows * width, dtype=np.uint8)
+    r = row0
+    while r < row0 + rows:
+        b = r // block_rows
+        blk = gen(width, block_rows, seed0 + b).pixels
+        lo = r - b * block_rows
+        hi = min(block_rows, row0 + rows - b * block_rows)
+        out[(r - row0) * width:(r - row0 + hi - lo) * width] = blk[lo * width:hi * width]
+        r += hi - lo
+    return out
+
+
+class Plan:
+    """What this rank holds and computes for a workload at world size N."""
+
+    def __init__(self, wl, world, rank, tf, D):
+        cfg = WORKLOADS[wl]
+        self.wl, self.cfg = wl, cfg
+        self.width = cfg["width"]
+        self.levels_list = cfg["levels"]
+        angles = cfg.get("angles", ANGLES)
+        self.dts = [(d, a) for d in cfg["ds"] for a in angles]
+        self.kinds = cfg["kinds"]
+        self.layout = cfg["layout"]
+        self.halo = D.halo_rows(self.dts) if self.layout.startswith("rows") else 0
+        self.bands = 1
+        if self.layout == "rows-weak":
+            self.height = cfg["block_rows"] * world          # global image
+            self.owned0, self.owned = rank * cfg["block_rows"], cfg["block_rows"]
+            self.gen_block = cfg["block_rows"]
+        elif self.layout == "rows-strong":
+            self.height = cfg["height"]
+            spec = D.shard_rows(self.width, self.height, self.dts, self.levels_list[0], world, rank) \
+                if world > 1 else None
+            self.owned0 = spec.owned_row_start if spec else 0
+            self.owned = spec.owned_rows() if spec else self.height
+            self.gen_block = GEN_BLOCK
+        elif self.layout == "bands":
+            self.height = cfg["height"]
+            self.band_ids = list(D.bands_for_rank(cfg["bands"], world, rank))
+            self.bands = len(self.band_ids)
+            self.owned0, self.owned = 0, self.height
+        else:  # replica
+            self.height = cfg["height"]
+            self.owned0, self.owned = 0, self.height
+        self.world, self.rank = world, rank
+        self.scaling = "weak" if self.layout in ("rows-weak", "replica") else "strong"
+
+    def buffer_rows_alloc(self):
+        return self.owned + (self.halo if self.layout.startswith("rows") else 0)
+
+    def pairs_per_step(self):
+        """Valid pairs of every GLCM the WHOLE job computes in one step."""
+        p = 0
+        for _L in self.levels_list:
+            for _k in self.kinds:
+                for d, a in self.dts:
+                    if self.layout == "bands":
+                        p += self.cfg["bands"] * valid_pairs(self.width, self.height, d, a)
+                    elif self.layout == "replica":
+                        p += self.world * valid_pairs(self.width, self.height, d, a)
+                    else:
+                        p += valid_pairs(self.width, self.height, d, a)
+        return p
+
+    def describe(self):
+        c = self.cfg
+        kinds = "+".join(self.kinds)
+        Ls = "/".join(str(x) for x in self.levels_list)
+        th = "/".join(str(a) for a in c.get("angles", ANGLES))
+        if self.layout == "rows-weak":
+            return (f"{self.wl}: {self.height}x{self.width} ({self.world} x {c['block_rows']}-row blocks) {kinds}, "
+                    f"L={Ls}, d={list(c['ds'])}, theta={th}, device-resident; row-partitioned, one {c['block_rows']}"
+                    f"x{self.width} block + {self.halo}-row halo per GPU, one NCCL reduce per step")
+        if self.layout == "rows-strong":
+            return (f"{self.wl}: {self.height}x{self.width} {kinds}, L={Ls}, d={list(c['ds'])}, theta={th}, "
+                    f"device-resident; row-partitioned over {self.world} GPU(s) with {self.halo}-row halos, "
+                    f"one NCCL reduce per step")
+        if self.layout == "bands":
+            return (f"{self.wl}: {c['bands']} bands of {self.width}x{self.height} {kinds}, L={Ls}, d={list(c['ds'])},"
+                    f" theta={th}, device-resident; bands sharded over {self.world} GPU(s), one launch per theta")
+        return (f"{self.wl}: {self.width}x{self.height} {kinds}, L={Ls}, d={list(c['ds'])}, theta={th}, "
+                f"device-resident, replica per GPU")
+
+
+def make_host_inputs(plan, tf):
+    """Pinned-able numpy buffers for this rank: {kind: array}. Rows layouts:
+    owned rows only (the halo arrives over NCCL). Bands: concatenated bands."""
+    imgs = {}
+    for kind in plan.kinds:
+        if plan.layout == "bands":
+            imgs[kind] = np.concatenate([tf.synth_noise(plan.width, plan.height, b + 1).pixels
+                                         for b in plan.band_ids])
+        elif plan.layout.startswith("rows"):
+            imgs[kind] = gen_rows(tf, kind, plan.width, plan.owned0, plan.owned, plan.gen_block, 1)
+        else:
+            gen = tf.synth_noise if kind == "noise" else tf.synth_smooth
+            imgs[kind] = gen(plan.width, plan.height, 1).pixels
+    return imgs
+
+
 # --------------------------------------------------------------------------- reference arm
-def cpu_reference_rate(imgs, n, levels, dts, seconds_budget, threads, n_bands=1, rotate=0):
-    """Times the reference's own compute_glcm_privatized (all host threads) on a
-    bounded sample: GLCMs over (image, (d, theta)) pairs until the budget."""
-    from oracle import oracle as O
-    r = O.ref()
-    handles = {}
-    for kind, px in imgs.items():
-        band = px[: n * n]
-        handles[kind] = r.ref_image_new(band.ctypes.data_as(C.POINTER(C.c_uint8)), n, n, levels)
-    out = np.zeros(levels * levels, dtype=np.uint64)
-    pairs, elapsed, calls = 0, 0.0, 0
-    jobs = [(k, d, a) for (d, a) in dts for k in imgs]
-    i = rotate
-    while elapsed < seconds_budget or calls < 2:
-        kind, d, a = jobs[i % len(jobs)]
-        i += 1
-        t = time.perf_counter()
-        rc = r.ref_image_glcm(handles[kind], d, a, threads, 1, out.ctypes.data_as(C.POINTER(C.c_uint64)))
-        elapsed += time.perf_counter() - t
-        assert rc == 0
-        pairs += valid_pairs(n, n, d, a)
-        calls += 1
-    for h in handles.values():
-        r.ref_image_free(h)
-    return pairs / elapsed / 1e9, calls
+def ref_image(r, gray, w, h, L):
+    """A reference QuantizedImage: the reference's own quantize(gray, L)
+    (image.hpp:55-62), untimed like in its CLI bench (texforge.cpp:190-236)."""
+    q = np.empty(w * h, dtype=np.uint8)
+    rc = r.ref_quantize(gray.ctypes.data_as(C.POINTER(C.c_uint8)), w, h, L, q.ctypes.data_as(C.POINTER(C.c_uint8)))
+    if rc:
+        raise RuntimeError("reference quantize failed")
+    hd = r.ref_image_new(q.ctypes.data_as(C.POINTER(C.c_uint8)), w, h, L)
+    if not hd:
+        raise RuntimeError("reference QuantizedImage construction failed")
+    return hd
 
 
 def run_reference(args, wl):
-    n, levels, ds, kinds, n_bands = WORKLOADS[wl]
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_1710_06189_b200 import texforge as tf
     from oracle import oracle as O
+    from paper_1710_06189_b200 import distributed as D
+    from paper_1710_06189_b200 import texforge as tf
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtexforge_ref.so not built"}))
         return
+    plan = Plan(wl, 1, 0, tf, D)
     threads = os.cpu_count() or 1
-    imgs = make_images(tf, n, kinds, 1, 0)
-    dts = [(d, a) for d in ds for a in ANGLES]
-    jobs = [(k, d, a) for (d, a) in dts for k in imgs]
+    w = plan.width
+    h = plan.height if plan.layout != "rows-weak" else plan.cfg["block_rows"]
+    if plan.layout == "rows-strong":
+        h = min(h, 8192)  # bounded sample: the first 8192 rows of the 65536^2 image
     r = O.ref()
-    handles = {k: r.ref_image_new(px.ctypes.data_as(C.POINTER(C.c_uint8)), n, n, levels) for k, px in imgs.items()}
-    out = np.zeros(levels * levels, dtype=np.uint64)
-    per_step = min(len(jobs), 2)  # bounded sample per step: one GLCM per input kind
+    imgs = {}
+    for kind in plan.kinds:
+        gen = tf.synth_noise if kind == "noise" else tf.synth_smooth
+        imgs[kind] = gen(w, h, 1).pixels
+    jobs = [(k, L, d, a) for L in plan.levels_list for (d, a) in plan.dts for k in plan.kinds]
+    handles = {(k, L): ref_image(r, imgs[k][: w * h], w, h, L) for k in plan.kinds for L in plan.levels_list}
+    outs = {L: np.zeros(L * L, dtype=np.uint64) for L in plan.levels_list}
+    per_step = min(len(jobs), 2)
 
     def step(s):
         p = 0
         for j in range(per_step):
-            kind, d, a = jobs[(s * per_step + j) % len(jobs)]
-            assert r.ref_image_glcm(handles[kind], d, a, threads, 1, out.ctypes.data_as(C.POINTER(C.c_uint64))) == 0
-            p += valid_pairs(n, n, d, a)
+            kind, L, d, a = jobs[(s * per_step + j) % len(jobs)]
+            assert r.ref_image_glcm(handles[(kind, L)], d, a, threads, 1,
+                                    outs[L].ctypes.data_as(C.POINTER(C.c_uint64))) == 0
+            p += valid_pairs(w, h, d, a)
         return p
 
     for s in range(args.warmup):
@@ -208,27 +320,54 @@ def run_reference(args, wl):
     pairs = sum(step(args.warmup + s) for s in range(args.steps))
     el = time.perf_counter() - t
     v = pairs / el / 1e9
-    sample = (f"{per_step} GLCMs/step (rotating over {len(jobs)} (input, d, theta) jobs) of the {n}x{n} "
-              f"L={levels} images; reference compute_glcm_privatized, {threads} workers")
+    sample = (f"{per_step} GLCMs/step, rotating over {len(jobs)} (input, L, d, theta) jobs, of {w}x{h} images; "
+              f"reference compute_glcm_privatized (unmodified headers), {threads} workers")
+    for hd in handles.values():
+        r.ref_image_free(hd)
     print(json.dumps({
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": f"{wl}: {n}x{n} {'+'.join(kinds)}, L={levels}, d={list(ds)}, theta=0/45/90/135",
-                   "host_threads": threads},
+        "scaling": plan.scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic", "impl": "reference",
+        "config": {"workload": plan.describe(), "host_threads": threads},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
-    for h in handles.values():
-        r.ref_image_free(h)
+
+
+def cpu_baseline(plan, imgs, seconds, threads):
+    """The reference's compute_glcm_privatized on all host threads, ~`seconds`
+    of work over (input, d, theta) GLCMs of this rank's images."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return None
+    r = O.ref()
+    w = plan.width
+    h = plan.owned if plan.layout != "bands" else plan.height
+    L = plan.levels_list[-1]
+    handles = {k: ref_image(r, v[: w * h], w, h, L) for k, v in imgs.items()}
+    out = np.zeros(L * L, dtype=np.uint64)
+    jobs = [(k, d, a) for (d, a) in plan.dts for k in imgs]
+    pairs, el, calls = 0, 0.0, 0
+    while el < seconds or calls < 2:
+        kind, d, a = jobs[calls % len(jobs)]
+        t = time.perf_counter()
+        assert r.ref_image_glcm(handles[kind], d, a, threads, 1, out.ctypes.data_as(C.POINTER(C.c_uint64))) == 0
+        el += time.perf_counter() - t
+        pairs += valid_pairs(w, h, d, a)
+        calls += 1
+    for hd in handles.values():
+        r.ref_image_free(hd)
+    return {"value": pairs / el / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{calls} single-(d,theta) GLCMs of {w}x{h} L={L} inputs (reference "
+                      f"compute_glcm_privatized, unmodified headers, {threads} workers, ~{seconds:.0f}s)"}
 
 
 # --------------------------------------------------------------------------- engine arm
 def run_engine(args, wl):
     import torch
 
-    from paper_1710_06189_b200 import _lib as L
+    from paper_1710_06189_b200 import _lib as Lb
+    from paper_1710_06189_b200 import distributed as D
     from paper_1710_06189_b200 import texforge as tf
 
     rank = int(os.environ.get("RANK", "0"))
@@ -240,141 +379,236 @@ def run_engine(args, wl):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    n, levels, ds, kinds, n_bands = WORKLOADS[wl]
+    plan = Plan(wl, world, rank, tf, D)
     eng = tf.Engine(local)
-    lib = L.load()
+    lib = Lb.load()
     t0 = time.time()
-    imgs = make_images(tf, n, kinds, n_bands, rank)
+    imgs = make_host_inputs(plan, tf)
     log(f"[rank {rank}] inputs ready in {time.time() - t0:.1f}s")
-    dts = [(d, a) for d in ds for a in ANGLES]
-    cells = levels * levels
-    dev = {k: torch.from_numpy(v).cuda() for k, v in imgs.items()}
-    n_out = len(kinds) * len(dts) * n_bands
-    acc = torch.zeros((n_out, cells), dtype=torch.int64, device="cuda")
+    W = plan.width
     stream = torch.cuda.current_stream()
     sptr = C.c_void_p(stream.cuda_stream)
-    pairs_per_step = sum(valid_pairs(n, n, d, a) for (d, a) in dts) * len(kinds) * n_bands
-    bytes_per_launch = n * n + cells * 8  # algorithmic: image read once + u64 GLCM write
 
-    launches = []  # (start_event, end_event) per hot-path call
+    # device-resident inputs: owned rows + halo (rows layouts; halo over NCCL)
+    dev, buf_rows = {}, {}
+    for kind, px in imgs.items():
+        alloc = plan.buffer_rows_alloc() * W if plan.layout != "bands" else px.size
+        t = torch.zeros(alloc + 64, dtype=torch.uint8, device="cuda")
+        t[: px.size].copy_(torch.from_numpy(px))
+        if plan.layout.startswith("rows") and world > 1:
+            buf_rows[kind] = D.exchange_halo(t, plan.owned, W, plan.halo, world, rank)
+        else:
+            buf_rows[kind] = plan.owned
+        dev[kind] = t
+    torch.cuda.synchronize()
+
+    jobs = [(L, kind, d, a) for L in plan.levels_list for kind in plan.kinds for (d, a) in plan.dts]
+    cells = {L: L * L for L in plan.levels_list}
+    out_off, o = [], 0
+    for (L, _k, _d, _a) in jobs:
+        out_off.append(o)
+        o += plan.bands * cells[L]
+    acc = torch.zeros(o, dtype=torch.int64, device="cuda")
+    pairs_per_step = plan.pairs_per_step()
+    flush = torch.empty(0, dtype=torch.uint8, device="cuda")
+    per_gpu_bytes = sum(v.numel() for v in dev.values())
+    if per_gpu_bytes < 2 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device="cuda")
+    launches = []
     record = {"on": False}
+
+    def vote_all():
+        for j, (L, kind, d, a) in enumerate(jobs):
+            if record["on"]:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            dst = C.c_void_p(acc.data_ptr() + out_off[j] * 8)
+            if plan.layout == "bands":
+                rc = lib.tfg_glcm_bands_async(eng.handle, C.c_void_p(dev[kind].data_ptr()), W, plan.height, W,
+                                              W * plan.height, plan.bands, 256, L, d, a, 0, dst, sptr)
+            else:
+                rc = lib.tfg_glcm_async(eng.handle, C.c_void_p(dev[kind].data_ptr()), W, buf_rows[kind], W,
+                                        plan.owned, 256, L, d, a, 0, dst, sptr)
+            if rc:
+                Lb.check(rc)
+            if record["on"]:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                launches.append((e0, e1))
 
     def step():
         acc.zero_()
-        o = 0
-        for kind in kinds:
-            base = dev[kind]
-            for b in range(n_bands):
-                for (d, a) in dts:
-                    if record["on"]:
-                        e0 = torch.cuda.Event(enable_timing=True)
-                        e0.record(stream)
-                    rc = lib.tfg_glcm_async(eng.handle, C.c_void_p(base.data_ptr() + b * n * n), n, n, n, n, 256,
-                                            levels, d, a, 0, C.c_void_p(acc[o].data_ptr()), sptr)
-                    if rc:
-                        L.check(rc)
-                    if record["on"]:
-                        e1 = torch.cuda.Event(enable_timing=True)
-                        e1.record(stream)
-                        launches.append((e0, e1))
-                    o += 1
+        vote_all()
+        if dist is not None and plan.layout.startswith("rows"):
+            dist.reduce(acc, dst=0, op=dist.ReduceOp.SUM)  # ONE NCCL reduce of every partial GLCM
 
-    # correctness gate on the first step (cheap: the L2-sized accumulators)
+    # correctness gate (first step, untimed): conservation on every GLCM, and
+    # the reference-generated Appendix-A hashes where the workload has them
     step()
     torch.cuda.synchronize()
-    for w_ in range(args.warmup):
+    check = {"conservation": None, "golden": None}
+    if rank == 0:
+        host = acc.cpu().numpy().view(np.uint64)
+        ok = True
+        for j, (L, kind, d, a) in enumerate(jobs):
+            for b in range(plan.bands):
+                seg = host[out_off[j] + b * cells[L]: out_off[j] + (b + 1) * cells[L]]
+                ok &= int(seg.sum()) == valid_pairs(W, plan.height, d, a)
+        check["conservation"] = bool(ok)
+        if wl == "c3" and world == 1:
+            with open(os.path.join(ROOT, "tests", "golden", "golden_hashes.json")) as f:
+                gold = {(g["kind"], g["size"], g["levels"], g["d"], g["theta"]): g["fnv"]
+                        for g in json.load(f)["glcm"]}
+            n_ok = n_all = 0
+            for j, (L, kind, d, a) in enumerate(jobs):
+                key = (kind, W, L, d, a)
+                if key in gold and d == 1:
+                    n_all += 1
+                    n_ok += fnv1a64(host[out_off[j]: out_off[j] + cells[L]]) == gold[key]
+            check["golden"] = f"{n_ok}/{n_all} Appendix-A FNV-1a hashes match"
+            ok &= n_ok == n_all
+        if not ok:
+            raise SystemExit(f"bench correctness gate failed: {check}")
+    for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
+
+    # timed region: K steps (L2 flushed between steps when the inputs fit in L2)
     l0 = eng.launches
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush_ms = 0.0
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
-        start.record(stream)
-        for s in range(args.steps):
-            step()
-        end.record(stream)
-        torch.cuda.synchronize()
+        if flush.numel():
+            fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            steps_ms = 0.0
+            for s in range(args.steps):
+                flush.fill_(s & 0xFF)
+                fe0.record(stream)
+                step()
+                fe1.record(stream)
+                torch.cuda.synchronize()
+                steps_ms += fe0.elapsed_time(fe1)
+            ms = steps_ms / args.steps
+        else:
+            start.record(stream)
+            for s in range(args.steps):
+                step()
+            end.record(stream)
+            torch.cuda.synchronize()
+            ms = start.elapsed_time(end) / args.steps
     gpu_launches = eng.launches - l0
-    ms = start.elapsed_time(end) / args.steps
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    value = world * pairs_per_step / (ms / 1e3) / 1e9
+    value = pairs_per_step / (ms / 1e3) / 1e9
 
-    # per-launch durations for the roofline (separate pass, same stream)
+    # per-call durations for the roofline (separate pass, same stream)
     record["on"] = True
     for s in range(max(2, min(args.steps, 5))):
-        step()
+        acc.zero_()
+        vote_all()
     torch.cuda.synchronize()
     durs = [a.elapsed_time(b) for a, b in launches]
     avg_ms = sum(durs) / len(durs)
     peak, peak_src = hbm_peak()
-    achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
+    bytes_per_call = sum(
+        (plan.bands * W * plan.height if plan.layout == "bands" else buf_rows[k] * W) + plan.bands * cells[L] * 8
+        for (L, k, _d, _a) in jobs) / len(jobs)
+    achieved = bytes_per_call / (avg_ms / 1e3) / 1e9
 
-    # end-to-end through the public API from pinned host memory
-    pinned = {k: torch.from_numpy(v).pin_memory() for k, v in imgs.items()}
-    probe = torch.empty(pinned[kinds[0]].numel(), dtype=torch.uint8, device="cuda")
-    h2d_gbs = []
-    for _ in range(3):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        probe.copy_(pinned[kinds[0]], non_blocking=True)
-        e1.record()
+    # end-to-end through the public C ABI from pinned host memory: H2D of this
+    # step's inputs inside the region, counts back to the host, NCCL reduce
+    e2e = None
+    if not args.no_e2e:
+        pinned = {}
+        for k, v in imgs.items():
+            rows = buf_rows[k] if plan.layout.startswith("rows") else None
+            src = dev[k][: rows * W].cpu() if rows is not None else torch.from_numpy(v)  # owned + halo rows
+            pinned[k] = src.pin_memory()
+        probe = torch.empty(pinned[plan.kinds[0]].numel(), dtype=torch.uint8, device="cuda")
+        h2d_gbs = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            probe.copy_(pinned[plan.kinds[0]], non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            h2d_gbs.append(probe.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        del probe
+        red = torch.zeros(o, dtype=torch.int64, device="cuda") if dist else None
+
+        def e2e_step():
+            parts = []
+            for L in plan.levels_list:
+                dts = plan.dts
+                for kind in plan.kinds:
+                    px = pinned[kind].numpy()
+                    if plan.layout == "bands":
+                        parts.append(eng.glcm(px, W, plan.height, L, dts, n_bands=plan.bands)
+                                     .transpose(1, 0, 2, 3).reshape(-1))
+                    else:
+                        parts.append(eng.shard(px, W, buf_rows[kind], plan.owned, L, dts).reshape(-1))
+            host = np.concatenate(parts)
+            if dist is not None and plan.layout.startswith("rows"):
+                red.copy_(torch.from_numpy(host.view(np.int64)))
+                dist.reduce(red, dst=0, op=dist.ReduceOp.SUM)
+                if rank == 0:
+                    host = red.cpu().numpy().view(np.uint64)
+            return host
+
+        e2e_step()
         torch.cuda.synchronize()
-        h2d_gbs.append(probe.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9)
-    del probe
-    e2e_steps = max(2, min(args.steps, 10))
-    h2d = sum(v.numel() for v in pinned.values())
-    d2h = n_out * cells * 8
-    eng.glcm(pinned[kinds[0]].numpy(), n, n, levels, dts[:1], n_bands=n_bands)  # warm the pinned ring
-    torch.cuda.synchronize()
-    t = time.perf_counter()
-    for s in range(e2e_steps):
-        for kind in kinds:
-            eng.glcm(pinned[kind].numpy(), n, n, levels, dts, n_bands=n_bands)
-    e2e_s = (time.perf_counter() - t) / e2e_steps
-    if dist:
-        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
-    e2e_value = world * pairs_per_step / e2e_s / 1e9
+        if dist:
+            dist.barrier()
+        n_e2e = max(2, min(args.steps, 10))
+        t = time.perf_counter()
+        for _ in range(n_e2e):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t) / n_e2e
+        if dist:
+            tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        h2d = sum(v.numel() for v in pinned.values()) * len(plan.levels_list)
+        e2e = {"value": pairs_per_step / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": world * h2d,
+               "d2h_bytes_per_step": world * o * 8,
+               "api": "tfg_glcm_shard / tfg_glcm_bands (pinned host input, Scheme-3 copy/vote stream pipeline, "
+                      "counts to host)" + (", + NCCL reduce" if dist else ""),
+               "pinned_h2d_GBps": max(h2d_gbs), "ms_per_step": e2e_s * 1e3,
+               "h2d_bound_ms_per_step": h2d / (max(h2d_gbs) * 1e9) * 1e3}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            from oracle import oracle as O
-            if O.ref_available():
-                threads = os.cpu_count() or 1
-                v, calls = cpu_reference_rate({k: v for k, v in imgs.items()}, n, levels, dts,
-                                              args.cpu_seconds, threads)
-                cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                       "sample": f"{calls} single-(d,theta) GLCMs of the {n}x{n} L={levels} inputs "
-                                 f"(reference compute_glcm_privatized, {threads} workers, ~{args.cpu_seconds:.0f}s)"}
-        except Exception as e:  # the baseline is reported, never required
+            cpu = cpu_baseline(plan, imgs, args.cpu_seconds, os.cpu_count() or 1)
+        except Exception as e:  # reported, never required
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {e}"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{wl}: {n}x{n}{' x' + str(n_bands) + ' bands' if n_bands > 1 else ''} "
-                                   f"{'+'.join(kinds)}, L={levels}, d={list(ds)}, theta=0/45/90/135, "
-                                   f"device-resident, one launch per (d,theta)",
-                       "pairs_per_step": pairs_per_step, "l2": "inputs (256 MiB each) larger than L2; no flush",
-                       "parallelism": f"replica x{world}"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": committed_traffic(wl),
-                         "kernel": "glcm_vote_kernel (+ glcm_reduce_partials_kernel for L*L > 4096)",
-                         "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms, "peak_source": peak_src},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "tfg_glcm (host pinned input, Scheme-3 stream pipeline, counts to host)",
-                    "pinned_h2d_GBps": max(h2d_gbs), "ms_per_step": e2e_s * 1e3,
-                    "h2d_bound_ms_per_step": h2d / (max(h2d_gbs) * 1e9) * 1e3},
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": plan.scaling,
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference synth_noise / synth_smooth generators)",
+            "config": {"workload": plan.describe(), "pairs_per_step": pairs_per_step,
+                       "glcms_per_step": len(jobs) * plan.bands * (world if plan.layout in ("bands", "replica")
+                                                                   else 1),
+                       "l2": ("inputs larger than L2 (126 MB); no flush" if not flush.numel()
+                              else "L2 flushed (256 MiB write) before every timed step; flush excluded"),
+                       "parallelism": {"rows-weak": f"row partition x{world} + NCCL reduce",
+                                       "rows-strong": f"row partition x{world} + NCCL reduce",
+                                       "bands": f"band shards x{world}", "replica": f"replica x{world}"}[plan.layout],
+                       "check": check},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": committed_traffic(wl),
+                         "kernel": "glcm_vote_kernel (+ its split-K partial reduce for L*L > 4096): one engine call",
+                         "bytes_per_launch": bytes_per_call, "avg_launch_ms": avg_ms, "peak_source": peak_src},
+            "e2e": e2e,
             "gpu_launches": gpu_launches,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
@@ -393,6 +627,7 @@ def main():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup raised to the contract minimum of 3")

@@ -4,7 +4,7 @@
  * This is the drop-in boundary beneath the reference's header-only C++ API
  * (R/ = /root/reference/proj/, namespace texforge). Every heavy reference
  * function maps to one entry point here; the C++ shim headers in
- * paper_1710_06189_b200/include/texforge/ and the Python mirror in
+ * include/texforge/ and the Python mirror in
  * paper_1710_06189_b200/texforge.py forward to these. Plain pointers and sizes
  * only: no C++ types, no torch types, no exceptions cross this boundary.
  *
@@ -136,6 +136,19 @@ int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height,
                    uint64_t* counts_out, double* probs_out, double* feats_out);
 
 /*
+ * One row shard of a larger image (the multi-GPU row partition,
+ * partition() semantics, pipeline.hpp:48-73): `px` holds `buffer_rows` rows,
+ * of which anchors in rows [0, owned_rows) vote; rows [owned_rows,
+ * buffer_rows) are the next shard's read-only halo. Host input streams
+ * through the Scheme-3 pipeline, device input (TFG_INPUT_DEVICE) votes in
+ * place. counts_out: n_dt*L*L u64 partial counts (host) for the caller's
+ * reduce (merge_chunk_glcms, pipeline.hpp:231-240, or one NCCL reduce).
+ */
+int tfg_glcm_shard(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t buffer_rows, size_t owned_rows,
+                   size_t pitch, int pixel_levels, int levels, const int* distances, const int* angles_deg,
+                   int n_dt, unsigned flags, uint64_t* counts_out);
+
+/*
  * Scheme 3 (compute_glcm_chunked, pipeline.hpp:246-337): K row chunks from
  * partition(), fetched by `fetch` into a pinned ring, H2D on a copy stream
  * overlapped with voting on the exec stream into one device accumulator.
@@ -171,10 +184,19 @@ int tfg_features(tfg_ctx* ctx, const double* probs, int levels, double* out5);
  * anchor rows (the owned rows of a shard; pass height for the whole image):
  * rows [row_end, height) are read-only halo, exactly like a ChunkSpec.
  * Used by the benchmark, the multi-GPU row shards and the parity tests.
+ * A context's async calls share its scratch (per-CTA partials), so they must
+ * be ordered on ONE stream (or the caller must serialise them).
  */
 int tfg_glcm_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t height, size_t pitch,
                    size_t row_end, int pixel_levels, int levels, int distance, int angle_deg,
                    unsigned flags, uint64_t* d_counts, void* stream);
+
+/* Multispectral batch on the device, one (d, theta), one launch (blockIdx.y =
+ * band): ADDS band b's GLCM into d_counts + b*L*L. Same stream rule as
+ * tfg_glcm_async: a context's async calls must be ordered on one stream. */
+int tfg_glcm_bands_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t height, size_t pitch,
+                         size_t band_stride, size_t n_bands, int pixel_levels, int levels, int distance,
+                         int angle_deg, unsigned flags, uint64_t* d_counts, void* stream);
 
 /* Device post-processing on `stream`: symmetrize (in place allowed? no: out != in). */
 int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned flags,

@@ -557,9 +557,12 @@ size_t auto_chunks(size_t width, size_t height, int max_d) {
 }
 
 // Chunk specs, partition() semantics (pipeline.hpp:48-73) with the largest
-// halo any requested (d, theta) needs.
+// halo any requested (d, theta) needs, over the owned anchor rows [0, height)
+// of a buffer of `total_rows` >= height rows (a row shard: the rows past
+// `height` are the next shard's halo and are read, never voted).
 std::vector<uint64_t> chunk_specs(size_t width, size_t height, const int* distances, const int* angles,
-                                  int n_dt, size_t k) {
+                                  int n_dt, size_t k, size_t total_rows = 0) {
+  if (total_rows < height) total_rows = height;
   int halo = 0, dmax = 1;
   for (int i = 0; i < n_dt; ++i) {
     dmax = std::max(dmax, distances[i]);
@@ -576,7 +579,7 @@ std::vector<uint64_t> chunk_specs(size_t width, size_t height, const int* distan
     const size_t end = row + base + (i < extra ? 1 : 0);
     s[3 * i] = row;
     s[3 * i + 1] = end;
-    s[3 * i + 2] = i + 1 == k ? end : std::min(height, end + (size_t)halo);
+    s[3 * i + 2] = std::min(total_rows, end + (size_t)halo);
     row = end;
   }
   return s;
@@ -588,8 +591,8 @@ std::vector<uint64_t> chunk_specs(size_t width, size_t height, const int* distan
 template <typename Fetch>
 void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, int levels,
                   const int* distances, const int* angles, int n_dt, size_t k, unsigned flags,
-                  unsigned long long* d_acc, Fetch&& fetch_rows) {
-  const std::vector<uint64_t> specs = chunk_specs(width, height, distances, angles, n_dt, k);
+                  unsigned long long* d_acc, Fetch&& fetch_rows, size_t total_rows = 0) {
+  const std::vector<uint64_t> specs = chunk_specs(width, height, distances, angles, n_dt, k, total_rows);
   const size_t pitch = round16(width);
   size_t max_rows = 0;
   for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, specs[3 * i + 2] - specs[3 * i]);
@@ -780,10 +783,13 @@ int tfg_quantize(tfg_ctx* ctx, const uint8_t* gray, size_t n, int levels, uint8_
   });
 }
 
-int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t pitch,
-                   size_t band_stride, size_t n_bands, int pixel_levels, int levels, const int* distances,
-                   const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out, double* probs_out,
-                   double* feats_out) {
+namespace {
+// One image (or n_bands images) of `height` buffer rows whose anchors in rows
+// [0, owned_rows) vote (owned_rows == height: the whole image).
+int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t owned_rows, size_t pitch,
+              size_t band_stride, size_t n_bands, int pixel_levels, int levels, const int* distances,
+              const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out, double* probs_out,
+              double* feats_out) {
   if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
   std::lock_guard<std::mutex> lk(ctx->mu);
   return guarded([&] {
@@ -795,10 +801,17 @@ int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height,
     if (n_bands > 1 && band_stride < pitch * height) fail(TFG_INVALID_ARGUMENT, "glcm: bands overlap");
     check_dts(distances, angles_deg, n_dt, width, height);
     if (!px) fail(TFG_INVALID_ARGUMENT, "glcm: null pixels");
+    if (owned_rows > height) fail(TFG_INVALID_ARGUMENT, "glcm: owned rows exceed the buffer rows");
     DeviceGuard dg(ctx->device);
     cudaStream_t s = ctx->exec;
     const size_t cells = (size_t)levels * levels;
     const size_t n_out = n_bands * (size_t)n_dt;
+    if (owned_rows == 0) {  // a shard that owns no anchors: zero counts
+      ck(cudaMemsetAsync(ctx->acc.get(n_out * cells * 8), 0, n_out * cells * 8, s), "memset");
+      finish(ctx, static_cast<unsigned long long*>(ctx->acc.p), (int)n_out, levels, flags & ~(TFG_NORMALIZE | TFG_FEATURES),
+             counts_out, nullptr, nullptr, s);
+      return;
+    }
     auto* d_acc = static_cast<unsigned long long*>(ctx->acc.get(n_out * cells * 8));
     ck(cudaMemsetAsync(d_acc, 0, n_out * cells * 8, s), "memset");
     const bool dev = (flags & TFG_INPUT_DEVICE) != 0;
@@ -807,7 +820,7 @@ int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height,
       // host image -> Scheme-3 stream pipeline (copy chunk i+1 while voting chunk i)
       int dmax = 1;
       for (int i = 0; i < n_dt; ++i) dmax = std::max(dmax, distances[i]);
-      const size_t k = auto_chunks(width, height, dmax);
+      const size_t k = auto_chunks(width, owned_rows, dmax);
       // per-(d,theta) accumulators are contiguous: d_acc + t*cells
       if (pitch != width) fail(TFG_INVALID_ARGUMENT, "glcm: host images must be dense (pitch == width)");
       // Pinned caller memory is DMA'd in place. Pageable memory would make
@@ -815,18 +828,20 @@ int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height,
       // first copied (by several host threads) into the pinned ring slot.
       const bool pageable = host_memory_kind(px) == 0;
       if (pageable) {
-        const std::vector<uint64_t> sp = chunk_specs(width, height, distances, angles_deg, n_dt, k);
+        const std::vector<uint64_t> sp = chunk_specs(width, owned_rows, distances, angles_deg, n_dt, k, height);
         size_t max_rows = 0;
         for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, sp[3 * i + 2] - sp[3 * i]);
         for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->hslot[sl].get(max_rows * width + 64);
       }
-      run_pipeline(ctx, width, height, pixel_levels, levels, distances, angles_deg, n_dt, k, flags, d_acc,
-                   [&](size_t, size_t start, size_t, size_t buf_end, int sl) -> const uint8_t* {
-                     if (!pageable) return px + start * width;
-                     uint8_t* dst = static_cast<uint8_t*>(ctx->hslot[sl].p);
-                     parallel_memcpy(dst, px + start * width, (buf_end - start) * width);
-                     return dst;
-                   });
+      run_pipeline(
+          ctx, width, owned_rows, pixel_levels, levels, distances, angles_deg, n_dt, k, flags, d_acc,
+          [&](size_t, size_t start, size_t, size_t buf_end, int sl) -> const uint8_t* {
+            if (!pageable) return px + start * width;
+            uint8_t* dst = static_cast<uint8_t*>(ctx->hslot[sl].p);
+            parallel_memcpy(dst, px + start * width, (buf_end - start) * width);
+            return dst;
+          },
+          height);
       if (pixel_levels == levels) check_async_flag(ctx, s);
       finish(ctx, d_acc, (int)n_out, levels, flags, counts_out, probs_out, feats_out, s);
       return;
@@ -853,13 +868,13 @@ int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height,
       // bands are batched in one launch (blockIdx.y = band); outputs band-major
       // [band][dt][cell]: launch per dt writing with a band stride of n_dt*cells.
       if (n_dt == 1) {
-        launch_vote(ctx, d_img, width, height, dpitch, dstride, (int)n_bands, height, pixel_levels, levels,
+        launch_vote(ctx, d_img, width, height, dpitch, dstride, (int)n_bands, owned_rows, pixel_levels, levels,
                     distances[t], angles_deg[t], flags, d_acc, s);
       } else {
         // per-dt scratch then scatter into band-major layout
         auto* tmp = static_cast<unsigned long long*>(ctx->tmp.get(n_bands * cells * 8));
         ck(cudaMemsetAsync(tmp, 0, n_bands * cells * 8, s), "memset");
-        launch_vote(ctx, d_img, width, height, dpitch, dstride, (int)n_bands, height, pixel_levels, levels,
+        launch_vote(ctx, d_img, width, height, dpitch, dstride, (int)n_bands, owned_rows, pixel_levels, levels,
                     distances[t], angles_deg[t], flags, tmp, s);
         ck(cudaMemcpy2DAsync(d_acc + (size_t)t * cells, (size_t)n_dt * cells * 8, tmp, cells * 8, cells * 8,
                              n_bands, cudaMemcpyDeviceToDevice, s),
@@ -869,6 +884,24 @@ int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height,
     if (pixel_levels == levels) check_async_flag(ctx, s);
     finish(ctx, d_acc, (int)n_out, levels, flags, counts_out, probs_out, feats_out, s);
   });
+}
+
+}  // namespace
+
+int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t pitch,
+                   size_t band_stride, size_t n_bands, int pixel_levels, int levels, const int* distances,
+                   const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out, double* probs_out,
+                   double* feats_out) {
+  return glcm_impl(ctx, px, width, height, height, pitch, band_stride, n_bands, pixel_levels, levels, distances,
+                   angles_deg, n_dt, flags, counts_out, probs_out, feats_out);
+}
+
+int tfg_glcm_shard(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t buffer_rows, size_t owned_rows,
+                   size_t pitch, int pixel_levels, int levels, const int* distances, const int* angles_deg, int n_dt,
+                   unsigned flags, uint64_t* counts_out) {
+  return glcm_impl(ctx, px, width, buffer_rows, owned_rows, pitch, pitch * buffer_rows, 1, pixel_levels, levels,
+                   distances, angles_deg, n_dt, flags & ~(TFG_SYMMETRIC | TFG_NORMALIZE | TFG_FEATURES), counts_out,
+                   nullptr, nullptr);
 }
 
 int tfg_glcm(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t pitch, int pixel_levels,
@@ -1083,6 +1116,28 @@ int tfg_glcm_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t heigh
     if (pixel_levels == levels) launch_validate(ctx, d_px, width, height, pitch, 0, 1, levels, ctx->d_err, s);
     launch_vote(ctx, d_px, width, height, pitch, 0, 1, row_end, pixel_levels, levels, distance, angle_deg, flags,
                 reinterpret_cast<unsigned long long*>(d_counts), s);
+  });
+}
+
+int tfg_glcm_bands_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t height, size_t pitch,
+                         size_t band_stride, size_t n_bands, int pixel_levels, int levels, int distance,
+                         int angle_deg, unsigned flags, uint64_t* d_counts, void* stream) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  return guarded([&] {
+    check_levels(levels, "glcm");
+    check_pixel_levels(pixel_levels, levels);
+    check_angle(angle_deg);
+    check_geometry(width, height, distance);
+    if ((reinterpret_cast<uintptr_t>(d_px) & 15) || (pitch % 16) || pitch < width || (band_stride % 16))
+      fail(TFG_INVALID_ARGUMENT, "glcm_async: device image must be 16-byte aligned with pitch % 16 == 0");
+    if (n_bands < 1 || n_bands > 65535) fail(TFG_INVALID_ARGUMENT, "glcm: band count must be in [1, 65535]");
+    if (n_bands > 1 && band_stride < pitch * height) fail(TFG_INVALID_ARGUMENT, "glcm: bands overlap");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (pixel_levels == levels)
+      launch_validate(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, levels, ctx->d_err, s);
+    launch_vote(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, height, pixel_levels, levels, distance,
+                angle_deg, flags, reinterpret_cast<unsigned long long*>(d_counts), s);
   });
 }
 

@@ -115,3 +115,34 @@ def engine_shard_compute(engine, device_image, width: int, height: int, pitch: i
         return acc
 
     return compute
+
+
+def halo_rows(dts: Sequence[Tuple[int, int]]) -> int:
+    """Rows of halo a shard needs below its owned rows (pipeline.hpp:60-61:
+    d for the downward angles, none at 0 degrees)."""
+    return max([d for d, a in dts if a != 0], default=0)
+
+
+def exchange_halo(slab, owned_rows: int, width: int, halo: int, world: int, rank: int):
+    """Completes each rank's read-only halo with one point-to-point exchange.
+
+    `slab` is a uint8 tensor of (owned_rows + halo) * width bytes whose first
+    owned_rows rows are this rank's rows of the global image (rank-major row
+    blocks). Rank r sends its first `halo` rows to rank r-1 and receives rank
+    r+1's first `halo` rows into its halo (NCCL over NVLink for CUDA tensors,
+    gloo for CPU tensors). The last rank owns the image's last rows and needs
+    no halo. Returns the number of valid buffer rows on this rank."""
+    import torch.distributed as dist
+
+    if halo == 0 or world == 1:
+        return owned_rows
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, slab[: halo * width].contiguous(), rank - 1))
+    recv = None
+    if rank + 1 < world:
+        recv = slab[owned_rows * width:(owned_rows + halo) * width]
+        ops.append(dist.P2POp(dist.irecv, recv, rank + 1))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    return owned_rows + (halo if rank + 1 < world else 0)

@@ -49,6 +49,24 @@ def _worker(rank, world, port, results):
             got = D.glcm_row_sharded(w, h, L, dts, compute, world, rank)
             want = np.stack([O.glcm_serial(q, w, h, L, d, a) for d, a in dts])
             out[(w, h, L)] = bool(np.array_equal(got, want))
+        # halo exchange: each rank starts with ONLY its own row block (the
+        # multi-GPU bench layout), receives the next block's first rows over
+        # the collective backend, votes its owned anchors, one reduce
+        import torch
+        w, L, blk = 45, 16, 23
+        dts = [(1, 0), (2, 45), (3, 90), (1, 135)]
+        halo = D.halo_rows(dts)
+        whole = O.quantize(tf.synth_noise(w, blk * world, 5).pixels, L)
+        slab = torch.zeros((blk + halo) * w, dtype=torch.uint8)
+        slab[: blk * w] = torch.from_numpy(whole[rank * blk * w:(rank + 1) * blk * w].copy())
+        rows = D.exchange_halo(slab, blk, w, halo, world, rank)
+        buf = slab.numpy()
+        part = np.zeros((len(dts), L * L), np.uint64)
+        for t, (d, a) in enumerate(dts):
+            O.glcm_rows(buf, w, rows, L, d, a, 0, blk, part[t])
+        got = D.reduce_partials(part.reshape(-1), all_ranks=True).reshape(len(dts), L * L)
+        want = np.stack([O.glcm_serial(whole, w, blk * world, L, d, a) for d, a in dts])
+        out["halo_exchange"] = bool(np.array_equal(got, want)) and rows == blk + (halo if rank + 1 < world else 0)
         # bands: contiguous blocks, every band exactly once
         owned = list(D.bands_for_rank(11, world, rank))
         gathered = [None] * world
