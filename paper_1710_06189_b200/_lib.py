@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtexforge_cuda.so")
+# TEXFORGE_CUDA_LIB: load another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("TEXFORGE_CUDA_LIB") or os.path.join(_HERE, "libtexforge_cuda.so")
 
 TFG_OK = 0
 TFG_INVALID_ARGUMENT = 1

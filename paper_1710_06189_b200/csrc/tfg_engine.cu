@@ -280,6 +280,21 @@ int floor_div(long a, long b) {
 
 // Geometry of one (d, theta) vote over a buffer of `height` rows of which
 // anchor rows [0, row_end) are owned (vote_anchor_rows, glcm.hpp:110-130).
+// CUTLASS-style FastDivmod constants: q = umulhi(n, mul) >> shr for n < 2^31
+// (d == 1: mul = 0, tfg::fast_div returns n).
+void fastdiv_consts(uint32_t dv, uint32_t* mul, uint32_t* shr) {
+  if (dv <= 1) {
+    *mul = 0;
+    *shr = 0;
+    return;
+  }
+  uint32_t l = 0;
+  while ((1ull << l) < dv) ++l;  // ceil(log2 d)
+  const uint32_t pw = 31 + l;
+  *mul = (uint32_t)(((1ull << pw) + dv - 1) / dv);
+  *shr = pw - 32;
+}
+
 struct VoteGeometry {
   tfg::VoteParams p{};
   int ksel = 4;
@@ -315,20 +330,21 @@ VoteGeometry make_geometry(size_t width, size_t height, size_t pitch, size_t row
   if (p.items >= (1ll << 31))
     fail(TFG_INVALID_ARGUMENT, "glcm: image too large for one launch (>= 2^31 16-pixel segments); split it into chunks");
   g.empty = p.items == 0 || p.col_end <= p.col_begin;
-  {
-    // CUTLASS-style FastDivmod constants: q = umulhi(n, mul) >> shr for n < 2^31
-    const uint32_t dv = (uint32_t)std::max(p.nch, 1);
-    if (dv == 1) {
-      p.div_mul = 0;
-      p.div_shr = 0;
-    } else {
-      uint32_t l = 0;
-      while ((1ull << l) < dv) ++l;  // ceil(log2 d)
-      const uint32_t pw = 31 + l;
-      p.div_mul = (uint32_t)(((1ull << pw) + dv - 1) / dv);
-      p.div_shr = pw - 32;
-    }
+  fastdiv_consts((uint32_t)std::max(p.nch, 1), &p.div_mul, &p.div_shr);
+  // two-pass split (glcm_vote_kernel): interior segments [1, nch-1) of every
+  // row run unmasked in the main pass; rows too narrow for 64-segment double
+  // batches go entirely through the edge pass
+  if (p.nch >= 66) {
+    p.ni = p.nch - 2;
+    p.ne = 2;
+  } else {
+    p.ni = 0;
+    p.ne = std::max(p.nch, 1);
   }
+  p.main_items = (long long)nrows * p.ni;
+  p.edge_items = (long long)nrows * p.ne;
+  fastdiv_consts((uint32_t)std::max(p.ni, 1), &p.ni_mul, &p.ni_shr);
+  fastdiv_consts((uint32_t)p.ne, &p.ne_mul, &p.ne_shr);
   // quantisation mode
   (void)pixel_levels;
   return g;
@@ -394,6 +410,8 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   per_band = std::min<long long>(per_band, (p.items + 2 * tfg::kThreads - 1) / (2 * tfg::kThreads));
   per_band = std::max<long long>(per_band, 1);
   p.items_per_cta = (p.items + per_band - 1) / per_band;
+  p.main_per_cta = ((p.main_items + per_band - 1) / per_band + 63) / 64 * 64;
+  p.edge_per_cta = (p.edge_items + per_band - 1) / per_band;
   const bool use_partials = cells > 4096;
   const bool packed_partials = use_partials && strat == tfg::S_PACKED16;
   if (use_partials) {

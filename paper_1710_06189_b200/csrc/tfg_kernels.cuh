@@ -76,6 +76,16 @@ struct VoteParams {
   unsigned long long* glcm;         // band b accumulator at glcm + b*L*L
   uint32_t* partials;               // null -> direct u64 atomics; else [band][grid][L*L]
   unsigned long long buf_bytes;     // bytes of one band buffer (rows * pitch): prefetch clamp
+  // two-pass decomposition (glcm_vote_kernel): interior segments j in [1, nch-1)
+  // of every anchor row (main pass, no masks) and the rest (edge pass)
+  int ni;                           // interior segments per row (0: everything is edge work)
+  uint32_t ni_mul, ni_shr;          // fast division by ni
+  long long main_items;             // nrows * ni
+  long long main_per_cta;           // multiple of 64
+  int ne;                           // edge segments per row (2, or nch when ni == 0)
+  uint32_t ne_mul, ne_shr;          // fast division by ne
+  long long edge_items;             // nrows * ne
+  long long edge_per_cta;
 };
 
 // ---------------------------------------------------------------------------
@@ -391,10 +401,19 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t 
 // ---------------------------------------------------------------------------
 // K1 + K2: fused quantise, vote, privatised merge.
 //
-// Work distribution inside a CTA is dynamic: a warp takes batch tickets from
-// a shared counter, so fast warps take more batches and no warp idles at the
-// final barrier. There is no barrier in the vote loop (PACKED16 included:
-// see kSpill).
+// Two passes over the CTA's share of the anchor raster:
+//  * main pass — the INTERIOR 16-pixel segments of every row (j in [1, nch-1)),
+//    flattened. Every reference byte of an interior segment lies inside its
+//    row, so these loads need no guards and all 16 pairs vote:
+//    no masks, no per-pair branches. A warp takes "double batches" of 64
+//    consecutive segments (lane and lane+32; each LDG.128 of the warp is one
+//    coalesced 512-byte access) from a per-CTA ticket counter, two per grab,
+//    and keeps two double batches in a register ring (one in flight while the
+//    other votes). Addresses come from one uniform division per double batch
+//    plus a per-lane row-wrap select.
+//  * edge pass — the first and last segment of every row (or every segment
+//    of a narrow image), with per-lane guarded loads and valid-anchor masks.
+// There is no barrier in either loop (PACKED16 included: see kSpill).
 template <int QUANT, int STRAT, int KSEL>
 __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams p) {
   extern __shared__ __align__(16) uint32_t hist[];
@@ -413,104 +432,139 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     const int n4 = p.hist_words >> 2;
     for (int i = tid; i < n4; i += kThreads) h4[i] = make_uint4(0, 0, 0, 0);
   }
-  if (tid == 0) s_ticket = 3 * kWarps;
 
   uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(hist));
   if constexpr (STRAT == S_COPIES32) hb += lane * 4u;
   if constexpr (STRAT == S_COPIES8) hb += (lane & 7u) * 4u;
 
-  const long long start64 = (long long)blockIdx.x * p.items_per_cta;
-  const long long end64 = min(start64 + p.items_per_cta, p.items);
-  const uint32_t start = (uint32_t)start64;
-  const uint32_t n_items = end64 > start64 ? (uint32_t)(end64 - start64) : 0u;
-  const uint32_t n_batches = (n_items + 31) / 32;
+  const uint32_t pitch = (uint32_t)p.pitch;
+  const uint32_t nch = (uint32_t)p.nch;
+  const uint32_t ni = (uint32_t)p.ni;
 
-  // Batch t = items [start + 32t, start + 32t + 32). The common case — all 32
-  // live, in one row, none at the row's edges — is decided once per warp
-  // (uniform) and costs no per-lane predicates: lane address = base + 16 lane.
-  auto issue_batch = [&](uint32_t t, RawItem& it) {
-    const uint32_t item0 = start + t * 32;
-    const uint32_t row0 = fast_div(item0, p.div_mul, p.div_shr);
-    const uint32_t j0 = item0 - row0 * (uint32_t)p.nch;
-    if ((t + 1) * 32 <= n_items && j0 >= 1 && j0 + 32 < (uint32_t)p.nch) {
-      const uint8_t* ap = band + (unsigned long long)row0 * (uint32_t)p.pitch + ((p.ch0 + j0 + lane) << 4);
-      it.a = ldg16(ap);
-      if constexpr (!ksel_c0_is_anchor<KSEL>()) it.c0 = ldg16(ap + p.ref_off);
-      if constexpr (ksel_needs_c1<KSEL>()) it.c1 = ldg16(ap + p.ref_off + 16);
-      it.mask = 0xFFFFu;
-    } else {
-      const uint32_t local = t * 32 + lane;
-      const uint32_t item = start + local;
-      const uint32_t row = fast_div(item, p.div_mul, p.div_shr);
-      const uint32_t j = item - row * (uint32_t)p.nch;
-      issue_item<KSEL>(p, band, row, j, t < n_batches && local < n_items, it);
-    }
-  };
-  // Every 32nd ticket also pulls the reference bytes (the leading edge of the
-  // stream) of batches [t+96, t+128) into L2, ahead of the register ring.
-  const uint32_t ticket_addr = static_cast<uint32_t>(__cvta_generic_to_shared(&s_ticket));
-  auto prefetch_ahead = [&](uint32_t tn) {
-    if ((tn & 31u) == 0 && tn + 96 < n_batches && lane == 0) {
-      const uint32_t i0 = start + (tn + 96) * 32;
-      const uint32_t i1 = start + min(n_items, (tn + 128) * 32) - 1;
-      const uint32_t r0 = fast_div(i0, p.div_mul, p.div_shr), r1 = fast_div(i1, p.div_mul, p.div_shr);
-      long long a0 = (long long)r0 * (long long)p.pitch + ((p.ch0 + (i0 - r0 * (uint32_t)p.nch)) << 4) + p.ref_off;
-      long long a1 = (long long)r1 * (long long)p.pitch + ((p.ch0 + (i1 - r1 * (uint32_t)p.nch)) << 4) + p.ref_off + 32;
-      a0 = max(a0, 0ll);
-      a1 = min(a1, (long long)p.buf_bytes);
-      if (a1 > a0) prefetch_l2(band + a0, (uint32_t)min(a1 - a0, 1ll << 20) & ~15u);
-    }
-  };
-  // Tickets come in triples (one shared atomic per revolution of the ring).
-  auto grab3 = [&]() -> uint32_t {
-    uint32_t tn = 0;
-    if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 3;" : "=r"(tn) : "r"(ticket_addr) : "memory");
-    tn = __shfl_sync(0xffffffffu, tn, 0);
-    prefetch_ahead(tn);
-    prefetch_ahead(tn + 1);
-    prefetch_ahead(tn + 2);
-    return tn;
-  };
-
-  // 3-slot register ring: batch k votes in place in its slot while batches
-  // k+1 and k+2 are in flight; the slot is refilled with batch k+3 after.
-  uint32_t t0 = 3 * warp, t1 = 3 * warp + 1, t2 = 3 * warp + 2;
-  RawItem n0, n1, n2;
-  issue_batch(t0, n0);
-  issue_batch(t1, n1);
-  issue_batch(t2, n2);
-  __syncthreads();  // histogram zeroed, ticket counter set
-
-  bool rle = true;  // run-length check on; re-sampled every 8th batch when it stops paying
+  bool rle = true;  // PACKED16 run-length check; re-sampled every 8th item when it stops paying
   uint32_t nb = 0;
-  auto process = [&](const RawItem& cur, uint32_t t) {
+  // Votes one item (16 pairs, or the pairs in `mask`).
+  auto vote_item = [&](const RawItem& cur) {
     uint32_t A[4], R[4], P[4], Q[4];
     ref_words<KSEL>(p, cur, A, R);
     prep_words<QUANT, STRAT>(p, A, R, P, Q);
-    const bool check = rle || (nb & 7) == 0;
-    bool fixed = false;
-    const bool hit = vote16<STRAT>(hb, P, Q, cur.mask, check, glcm, L, fixed);
-    if (check) rle = __popc(__ballot_sync(0xffffffffu, hit)) >= 4;  // >= 1/8 of the warp's segments
-    // PACKED16: this warp's fix-ups happen-before its next item's atomics
     if constexpr (STRAT == S_PACKED16) {
+      const bool check = rle || (nb & 7) == 0;
+      bool fixed = false;
+      const bool hit = vote16<STRAT>(hb, P, Q, cur.mask, check, glcm, L, fixed);
+      if (check) rle = __popc(__ballot_sync(0xffffffffu, hit)) >= 4;
+      // this warp's fix-ups happen-before its next item's atomics
       if (__any_sync(0xffffffffu, fixed)) __syncwarp();
+      ++nb;
+    } else if (cur.mask == 0xFFFFu) {
+      // conflict-free (COPIES*) or hardware-aggregated (COPY1: POPC.INC) layouts
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) red_smem1(vote_addr<STRAT>(hb, pair_x(P[i], Q[i], k)));
+    } else if (cur.mask) {
+      vote_masked<STRAT>(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], cur.mask, glcm, L);
     }
-    ++nb;
   };
+
+  // ---------------- main pass: interior segments, 64 per double batch -------
+  const long long mbeg64 = (long long)blockIdx.x * p.main_per_cta;
+  const long long mend64 = min(mbeg64 + p.main_per_cta, p.main_items);
+  const uint32_t mbeg = (uint32_t)mbeg64;
+  const uint32_t m_items = mend64 > mbeg64 ? (uint32_t)(mend64 - mbeg64) : 0u;
+  const uint32_t n_dbl = (m_items + 63) / 64;
+  const uint32_t wrap_off = pitch - ni * 16u;  // next row, back to interior segment 0
+
+  // double batch t -> items lane and lane+32 of [mbeg + 64t, +64)
+  auto issue_dbl = [&](uint32_t t, RawItem& x0, RawItem& x1) {
+    const uint32_t f0 = mbeg + t * 64;                       // warp-uniform
+    const uint32_t row0 = fast_div(f0, p.ni_mul, p.ni_shr);
+    const uint32_t jj0 = f0 - row0 * ni;
+    const uint8_t* base = band + (unsigned long long)row0 * pitch + ((p.ch0 + 1 + jj0) << 4);
+    const bool tail = (t + 1) * 64 > m_items;               // warp-uniform
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      RawItem& it = k ? x1 : x0;
+      const uint32_t d = lane + 32u * k;
+      const uint32_t jj = jj0 + d;
+      const uint32_t off = (jj >= ni ? wrap_off : 0u) + (d << 4);  // ni >= 64: at most one wrap
+      const uint8_t* ap = base + off;
+      it.mask = 0xFFFFu;
+      if (tail && t * 64 + d >= m_items) {
+        it.mask = 0;
+        continue;
+      }
+      it.a = ldg16(ap);
+      if constexpr (!ksel_c0_is_anchor<KSEL>()) it.c0 = ldg16(ap + p.ref_off);
+      if constexpr (ksel_needs_c1<KSEL>()) it.c1 = ldg16(ap + p.ref_off + 16);
+    }
+  };
+
+  const uint32_t ticket_addr = static_cast<uint32_t>(__cvta_generic_to_shared(&s_ticket));
+  // L2 bulk prefetch of the stream's leading edge (reference bytes of double
+  // batches [b0, b0 + nb)), issued by the grab that crosses a multiple of kSpan.
+  auto prefetch_span = [&](uint32_t b0, uint32_t nbat) {
+    if (b0 >= n_dbl) return;
+    const uint32_t i0 = mbeg + b0 * 64;
+    const uint32_t i1 = mbeg + min(m_items, (b0 + nbat) * 64) - 1;
+    const uint32_t r0 = fast_div(i0, p.ni_mul, p.ni_shr), r1 = fast_div(i1, p.ni_mul, p.ni_shr);
+    long long a0 = (long long)r0 * pitch + ((p.ch0 + 1 + (i0 - r0 * ni)) << 4) + p.ref_off;
+    long long a1 = (long long)r1 * pitch + ((p.ch0 + 1 + (i1 - r1 * ni)) << 4) + p.ref_off + 32;
+    a0 = max(a0, 0ll) & ~15ll;
+    a1 = min(a1, (long long)p.buf_bytes);
+    if (a1 > a0) prefetch_l2(band + a0, (uint32_t)min(a1 - a0, 1ll << 20) & ~15u);
+  };
+  constexpr uint32_t kAhead = 48, kSpan = 16;
+  auto grab2 = [&]() -> uint32_t {
+    uint32_t tn = 0;
+    if (lane == 0) {
+      asm volatile("atom.shared.add.u32 %0, [%1], 2;" : "=r"(tn) : "r"(ticket_addr) : "memory");
+      if (((tn + 1) & (kSpan - 1)) < 2) prefetch_span(((tn + 1) & ~(kSpan - 1)) + kAhead, kSpan);
+    }
+    return __shfl_sync(0xffffffffu, tn, 0);
+  };
+
+  RawItem a0, a1, b0i, b1i;
+  uint32_t ta = 2 * warp, tb = 2 * warp + 1;
+  if (ta < n_dbl) issue_dbl(ta, a0, a1);
+  if (tb < n_dbl) issue_dbl(tb, b0i, b1i);
+  if (tid == 0) {
+    s_ticket = 2 * kWarps;
+    for (uint32_t q = 0; q < kAhead + kSpan; q += kSpan) prefetch_span(q + 2 * kWarps, kSpan);
+  }
+  __syncthreads();  // histogram zeroed, ticket counter set
+
   for (;;) {
-    if (t0 >= n_batches) break;
-    process(n0, t0);
-    const uint32_t tn = grab3();
-    t0 = tn;
-    issue_batch(t0, n0);
-    if (t1 >= n_batches) break;
-    process(n1, t1);
-    t1 = tn + 1;
-    issue_batch(t1, n1);
-    if (t2 >= n_batches) break;
-    process(n2, t2);
-    t2 = tn + 2;
-    issue_batch(t2, n2);
+    if (ta >= n_dbl) break;
+    vote_item(a0);
+    vote_item(a1);
+    const uint32_t tn = grab2();
+    ta = tn;
+    if (ta < n_dbl) issue_dbl(ta, a0, a1);
+    if (tb >= n_dbl) break;
+    vote_item(b0i);
+    vote_item(b1i);
+    tb = tn + 1;
+    if (tb < n_dbl) issue_dbl(tb, b0i, b1i);
+  }
+
+  // ---------------- edge pass: first/last segment of each row (or all) -----
+  {
+    const long long ebeg64 = (long long)blockIdx.x * p.edge_per_cta;
+    const long long eend64 = min(ebeg64 + p.edge_per_cta, p.edge_items);
+    const uint32_t ebeg = (uint32_t)ebeg64;
+    const uint32_t e_items = eend64 > ebeg64 ? (uint32_t)(eend64 - ebeg64) : 0u;
+    const uint32_t ne = (uint32_t)p.ne;
+    for (uint32_t t = warp; t * 32 < e_items; t += kWarps) {
+      const uint32_t local = t * 32 + lane;
+      const uint32_t e = ebeg + local;
+      const uint32_t row = fast_div(e, p.ne_mul, p.ne_shr);
+      const uint32_t r = e - row * ne;
+      const uint32_t j = ni ? (r ? nch - 1 : 0u) : r;
+      RawItem it;
+      issue_item<KSEL>(p, band, row, j, local < e_items, it);
+      vote_item(it);
+    }
   }
   __syncthreads();
 

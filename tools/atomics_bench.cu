@@ -88,6 +88,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT, 1) dsmem_bench(u
   if (threadIdx.x == 0) atomicMax(cycles, t1 - t0);
 }
 
+// Global (L2) atomics: red.global.add.u32 on random words of a region that is
+// either private per CTA (`priv` words each) or shared by all CTAs.
+template <bool shared_region>
+__global__ void __launch_bounds__(kT, 1) gbench(unsigned long long* cycles, uint32_t* g, uint32_t words) {
+  uint32_t h = threadIdx.x * 0x9E3779B9u + blockIdx.x * 0x85EBCA6Bu;
+  uint32_t* base = shared_region ? g : g + (size_t)blockIdx.x * words;
+  const unsigned long long t0 = clock64();
+#pragma unroll 8
+  for (int k = 0; k < kIters / 4; ++k) {
+    h = h * 1664525u + 1013904223u;
+    const uint32_t r = (h >> 7) ^ (h >> 19);
+    asm volatile("red.global.add.u32 [%0], 1;" ::"l"(base + (r % words)) : "memory");
+  }
+  const unsigned long long t1 = clock64();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(cycles, t1 - t0);
+}
+
 int main() {
   int dev = 0, sms = 0, clk = 0;
   cudaGetDevice(&dev);
@@ -139,6 +157,27 @@ int main() {
     const double ops = (double)sms * kT * kIters;
     printf(", \"%s\": {\"ms\": %.4f, \"Gops_s\": %.1f, \"ops_per_clk_per_sm\": %.3f}", dn[m], ms, ops / ms / 1e6,
            (double)kT * kIters / (double)c);
+  }
+  {
+    uint32_t* g;
+    const uint32_t words = 8192;
+    cudaMalloc(&g, (size_t)sms * words * 4);
+    using G = void (*)(unsigned long long*, uint32_t*, uint32_t);
+    G gs[2] = {gbench<false>, gbench<true>};
+    const char* gn[2] = {"l2_red_private_8K", "l2_red_shared_8K"};
+    for (int m = 0; m < 2; ++m) {
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaMemset(cyc, 0, 8);
+        cudaEventRecord(a);
+        gs[m]<<<sms, kT>>>(cyc, g, words);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+      }
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      const double ops = (double)sms * kT * (kIters / 4);
+      printf(", \"%s\": {\"ms\": %.4f, \"Gops_s\": %.1f}", gn[m], ms, ops / ms / 1e6);
+    }
   }
   printf("}, \"err\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
