@@ -44,7 +44,7 @@ enum Strat : int {
   S_COPIES8 = 2,   // L <= 64:  8 u32 copies [b + 64a][lane%8]; P = 4b, Q = a, addr = 8x + 4 (lane%8)
   S_COPY1 = 3,     // L <= 128: 1 u32 copy [a + 128b]; P = 2a, Q = b, addr = 2x
   S_PACKED16 = 4   // L <= 256: 1 copy of u16 counters, cell a + 256b in word (x & 0x7fff), half b >> 7,
-                   //           spilled to the u64 cell every kSpill votes
+                   //           drained to the u64 cells past 2^15 (kDrainBit)
 };
 
 __host__ __device__ constexpr int strat_scale(int s) {  // log2 of the P-byte scale
@@ -177,77 +177,78 @@ __device__ __forceinline__ uint32_t packed_inc(uint32_t Q, int j) {
   return prmt(Q, 0u, 0x4400u | ((8u + j) << 4) | (8u + j)) + 1u;
 }
 
-// PACKED16 spill rule (no barriers). A field spills kSpill = 2048 votes to
-// the u64 cell each time it crosses a multiple of kSpill: the crossing atomic
-// sees it exactly ((old ^ new) changes a bit >= 11 of its field) and its
-// thread subtracts kSpill. Every fix-up lowers the field across exactly one
-// multiple, so the crossings awaiting their fix-up on a field number exactly
-// floor(v / kSpill). A warp adds <= 512 to one field per item (32 lanes x 16)
-// and fences its fix-ups before its next item, so it holds <= 1 pending
-// crossing per field: v < (warps + 1) * kSpill = 25 * 2048 = 51200 < 2^16.
-constexpr uint32_t kSpill = 2048;
-static_assert((kThreads / 32 + 1) * kSpill + 512 <= 65535, "PACKED16 field bound");
+// PACKED16 overflow rule (exact, no barriers, no per-vote ownership test).
+// Every PACKED16 vote is a returning atomic and its thread ORs the returned
+// word into a per-item flag. When a field has reached 2^15 (bit 15 of either
+// half set) the thread DRAINS every word it voted in that item: one
+// atomicAnd(word, 0x07FF07FF) takes ownership of all whole multiples of 2048
+// in both halves at once, and those counts go to the u64 cells. Because the
+// AND is atomic, every count is moved exactly once no matter how many
+// threads drain the same word. Bound: once a field passes 2^15, every warp
+// that votes on it sees bit 15 and drains before its next item, and a warp
+// adds <= 512 to one field per item (32 lanes x 16), so before the first
+// drain lands the field stays < 2^15 + 24 * 512 + 512 < 2^16.
+constexpr uint32_t kDrainBit = 0x80008000u;
+static_assert(32768u + (kThreads / 32 + 1) * 512u < 65536u, "PACKED16 field bound");
 
-__device__ __forceinline__ bool packed_crossed(uint32_t old, uint32_t inc) {
-  return ((old ^ (old + inc)) & 0xF800F800u) != 0;
+// Drains one PACKED16 word whose cell is x = a + 256 b (b's top bit selects
+// the half; the word holds cells (a, b&127) and (a, (b&127)+128)).
+__device__ __forceinline__ void packed_drain(uint32_t addr, uint32_t x, unsigned long long* glcm, uint32_t L) {
+  uint32_t old;
+  asm volatile("atom.shared.and.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(0x07FF07FFu) : "memory");
+  const uint32_t a = x & 0xFFu, b = (x >> 8) & 0x7Fu;
+  const uint32_t lo = old & 0xF800u, hi = (old >> 16) & 0xF800u;
+  if (lo) atomicAdd(glcm + b * L + a, (unsigned long long)lo);
+  if (hi) atomicAdd(glcm + (b + 128u) * L + a, (unsigned long long)hi);
 }
-__device__ __forceinline__ bool packed_fixup(uint32_t addr, uint32_t x, uint32_t old, uint32_t inc,
-                                             unsigned long long* glcm, uint32_t L) {
-  if (packed_crossed(old, inc)) {
-    red_smem(addr, 0u - ((inc & 0xFFFFu) ? kSpill : (kSpill << 16)));
-    atomicAdd(glcm + ((x >> 8) & 0xFFu) * L + (x & 0xFFu), (unsigned long long)kSpill);
-    return true;
+
+// Rare path, out of line so the hot loop fits the instruction cache: drain
+// the words of the pixels in `mask` of one item.
+__device__ __noinline__ void packed_drain_item(uint32_t hb, uint32_t P0, uint32_t P1, uint32_t P2, uint32_t P3,
+                                               uint32_t Q0, uint32_t Q1, uint32_t Q2, uint32_t Q3, uint32_t mask,
+                                               unsigned long long* glcm, uint32_t L) {
+  const uint32_t P[4] = {P0, P1, P2, P3}, Q[4] = {Q0, Q1, Q2, Q3};
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (mask & (1u << k)) {
+      const uint32_t x = pair_x(P[k >> 2], Q[k >> 2], k & 3);
+      packed_drain(vote_addr<S_PACKED16>(hb, x), x, glcm, L);
+    }
   }
-  return false;
 }
 
+// One vote of weight n; returns the old word for PACKED16 (else 0).
 template <int STRAT>
-__device__ __forceinline__ bool emit(uint32_t hb, uint32_t P, uint32_t Q, int j, uint32_t n,
-                                     unsigned long long* glcm, uint32_t L) {
-  const uint32_t x = pair_x(P, Q, j);
-  const uint32_t addr = vote_addr<STRAT>(hb, x);
+__device__ __forceinline__ uint32_t emit(uint32_t hb, uint32_t P, uint32_t Q, int j, uint32_t n) {
+  const uint32_t addr = vote_addr<STRAT>(hb, pair_x(P, Q, j));
   if constexpr (STRAT == S_PACKED16) {
-    const uint32_t inc = packed_inc(Q, j) * n;
-    return packed_fixup(addr, x, atom_smem(addr, inc), inc, glcm, L);
+    return atom_smem(addr, packed_inc(Q, j) * n);
   } else {
     red_smem(addr, n);
-    return false;
+    return 0u;
   }
-}
-
-// Rare paths live out of line so the hot loop fits the instruction cache.
-// Spill fix-ups of the 4 pixels of one word (PACKED16).
-__device__ __noinline__ bool packed_fix_word(uint32_t hb, uint32_t P, uint32_t Q, uint32_t o0, uint32_t o1,
-                                             uint32_t o2, uint32_t o3, unsigned long long* glcm, uint32_t L) {
-  const uint32_t old[4] = {o0, o1, o2, o3};
-  bool fixed = false;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t x = pair_x(P, Q, j);
-    fixed |= packed_fixup(vote_addr<S_PACKED16>(hb, x), x, old[j], packed_inc(Q, j), glcm, L);
-  }
-  return fixed;
 }
 
 // Edge segments of a row: only the anchors in `mask` vote.
 template <int STRAT>
-__device__ __noinline__ bool vote_masked(uint32_t hb, uint32_t P0, uint32_t P1, uint32_t P2, uint32_t P3,
+__device__ __noinline__ void vote_masked(uint32_t hb, uint32_t P0, uint32_t P1, uint32_t P2, uint32_t P3,
                                          uint32_t Q0, uint32_t Q1, uint32_t Q2, uint32_t Q3, uint32_t mask,
                                          unsigned long long* glcm, uint32_t L) {
   const uint32_t P[4] = {P0, P1, P2, P3}, Q[4] = {Q0, Q1, Q2, Q3};
-  bool fixed = false;
+  uint32_t flag = 0;
 #pragma unroll
   for (int k = 0; k < 16; ++k)
-    if (mask & (1u << k)) fixed |= emit<STRAT>(hb, P[k >> 2], Q[k >> 2], k & 3, 1u, glcm, L);
-  return fixed;
+    if (mask & (1u << k)) flag |= emit<STRAT>(hb, P[k >> 2], Q[k >> 2], k & 3, 1u);
+  if constexpr (STRAT == S_PACKED16) {
+    if (flag & kDrainBit) packed_drain_item(hb, P0, P1, P2, P3, Q0, Q1, Q2, Q3, mask, glcm, L);
+  }
 }
 
 // Votes the 16 pixel pairs of one item. Returns true when the run-length
 // shortcut fired (all 16 pairs identical: one vote of weight 16).
 template <int STRAT>
 __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], const uint32_t (&Q)[4],
-                                       uint32_t mask, bool rle, unsigned long long* glcm, uint32_t L,
-                                       bool& fixed) {
+                                       uint32_t mask, bool rle, unsigned long long* glcm, uint32_t L) {
   if (mask == 0xFFFFu) {
     if (rle) {
       // smooth inputs (95-99.7% of neighbouring pairs repeat)
@@ -255,25 +256,22 @@ __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], cons
       const uint32_t diff = (P[0] ^ bp) | (P[1] ^ bp) | (P[2] ^ bp) | (P[3] ^ bp) | (Q[0] ^ bq) |
                             (Q[1] ^ bq) | (Q[2] ^ bq) | (Q[3] ^ bq);
       if (diff == 0) {
-        fixed |= emit<STRAT>(hb, P[0], Q[0], 0, 16u, glcm, L);
+        const uint32_t old = emit<STRAT>(hb, P[0], Q[0], 0, 16u);
+        if constexpr (STRAT == S_PACKED16) {
+          if (old & kDrainBit) packed_drain_item(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], 1u, glcm, L);
+        }
         return true;
       }
     }
     if constexpr (STRAT == S_PACKED16) {
-      // 4 atomics (one word) back to back, then their spill checks
+      uint32_t flag = 0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        uint32_t old[4], inc[4];
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          inc[j] = packed_inc(Q[i], j);
-          old[j] = atom_smem(vote_addr<STRAT>(hb, pair_x(P[i], Q[i], j)), inc[j]);
-        }
-        uint32_t flag = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) flag |= old[j] ^ (old[j] + inc[j]);
-        if (flag & 0xF800F800u) fixed |= packed_fix_word(hb, P[i], Q[i], old[0], old[1], old[2], old[3], glcm, L);
-      }
+        for (int j = 0; j < 4; ++j)
+          flag |= atom_smem(vote_addr<STRAT>(hb, pair_x(P[i], Q[i], j)), packed_inc(Q[i], j));
+      if (flag & kDrainBit)
+        packed_drain_item(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], 0xFFFFu, glcm, L);
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -281,12 +279,10 @@ __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], cons
         for (int j = 0; j < 4; ++j) red_smem1(vote_addr<STRAT>(hb, pair_x(P[i], Q[i], j)));
     }
   } else if (mask) {
-    fixed |= vote_masked<STRAT>(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], mask, glcm, L);
+    vote_masked<STRAT>(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], mask, glcm, L);
   }
   return false;
 }
-
-
 
 // Layout position (in counters) of real cell (ref b, anchor a).
 template <int STRAT>
@@ -413,7 +409,7 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t 
 //    plus a per-lane row-wrap select.
 //  * edge pass — the first and last segment of every row (or every segment
 //    of a narrow image), with per-lane guarded loads and valid-anchor masks.
-// There is no barrier in either loop (PACKED16 included: see kSpill).
+// There is no barrier in either loop (PACKED16 included: see kDrainBit).
 template <int QUANT, int STRAT, int KSEL>
 __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams p) {
   extern __shared__ __align__(16) uint32_t hist[];
@@ -450,11 +446,8 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     prep_words<QUANT, STRAT>(p, A, R, P, Q);
     if constexpr (STRAT == S_PACKED16) {
       const bool check = rle || (nb & 7) == 0;
-      bool fixed = false;
-      const bool hit = vote16<STRAT>(hb, P, Q, cur.mask, check, glcm, L, fixed);
+      const bool hit = vote16<STRAT>(hb, P, Q, cur.mask, check, glcm, L);
       if (check) rle = __popc(__ballot_sync(0xffffffffu, hit)) >= 4;
-      // this warp's fix-ups happen-before its next item's atomics
-      if (__any_sync(0xffffffffu, fixed)) __syncwarp();
       ++nb;
     } else if (cur.mask == 0xFFFFu) {
       // conflict-free (COPIES*) or hardware-aggregated (COPY1: POPC.INC) layouts
@@ -464,6 +457,24 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
         for (int k = 0; k < 4; ++k) red_smem1(vote_addr<STRAT>(hb, pair_x(P[i], Q[i], k)));
     } else if (cur.mask) {
       vote_masked<STRAT>(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], cur.mask, glcm, L);
+    }
+  };
+
+  // An unmasked item of the main pass (all 16 pairs vote).
+  auto vote_full = [&](const RawItem& cur) {
+    uint32_t A[4], R[4], P[4], Q[4];
+    ref_words<KSEL>(p, cur, A, R);
+    prep_words<QUANT, STRAT>(p, A, R, P, Q);
+    if constexpr (STRAT == S_PACKED16) {
+      const bool check = rle || (nb & 7) == 0;
+      const bool hit = vote16<STRAT>(hb, P, Q, 0xFFFFu, check, glcm, L);
+      if (check) rle = __popc(__ballot_sync(0xffffffffu, hit)) >= 4;
+      ++nb;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) red_smem1(vote_addr<STRAT>(hb, pair_x(P[i], Q[i], k)));
     }
   };
 
@@ -515,11 +526,11 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     if (a1 > a0) prefetch_l2(band + a0, (uint32_t)min(a1 - a0, 1ll << 20) & ~15u);
   };
   constexpr uint32_t kAhead = 48, kSpan = 16;
-  auto grab2 = [&]() -> uint32_t {
+  auto grab4 = [&]() -> uint32_t {
     uint32_t tn = 0;
     if (lane == 0) {
-      asm volatile("atom.shared.add.u32 %0, [%1], 2;" : "=r"(tn) : "r"(ticket_addr) : "memory");
-      if (((tn + 1) & (kSpan - 1)) < 2) prefetch_span(((tn + 1) & ~(kSpan - 1)) + kAhead, kSpan);
+      asm volatile("atom.shared.add.u32 %0, [%1], 4;" : "=r"(tn) : "r"(ticket_addr) : "memory");
+      if (((tn + 3) & (kSpan - 1)) < 4) prefetch_span(((tn + 3) & ~(kSpan - 1)) + kAhead, kSpan);
     }
     return __shfl_sync(0xffffffffu, tn, 0);
   };
@@ -534,17 +545,35 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   }
   __syncthreads();  // histogram zeroed, ticket counter set
 
+  // Only the CTA's last double batch can be partial (warp-uniform test).
+  const uint32_t n_full_dbl = m_items / 64;
+  auto vote_dbl = [&](uint32_t t, const RawItem& x0, const RawItem& x1) {
+    if (t < n_full_dbl) {
+      vote_full(x0);
+      vote_full(x1);
+    } else {
+      vote_item(x0);
+      vote_item(x1);
+    }
+  };
+  // one ticket grab (4 double batches) per two revolutions of the ring
   for (;;) {
     if (ta >= n_dbl) break;
-    vote_item(a0);
-    vote_item(a1);
-    const uint32_t tn = grab2();
+    vote_dbl(ta, a0, a1);
+    const uint32_t tn = grab4();
     ta = tn;
     if (ta < n_dbl) issue_dbl(ta, a0, a1);
     if (tb >= n_dbl) break;
-    vote_item(b0i);
-    vote_item(b1i);
+    vote_dbl(tb, b0i, b1i);
     tb = tn + 1;
+    if (tb < n_dbl) issue_dbl(tb, b0i, b1i);
+    if (ta >= n_dbl) break;
+    vote_dbl(ta, a0, a1);
+    ta = tn + 2;
+    if (ta < n_dbl) issue_dbl(ta, a0, a1);
+    if (tb >= n_dbl) break;
+    vote_dbl(tb, b0i, b1i);
+    tb = tn + 3;
     if (tb < n_dbl) issue_dbl(tb, b0i, b1i);
   }
 
