@@ -113,6 +113,7 @@ struct tfg_ctx {
   DevBuf qbuf;                           // quantize in/out
   DevBuf tmp;                            // per-(d,theta) band scratch
   int* d_err = nullptr;                  // async error flag (+ per-GLCM flags)
+  unsigned int* sync_ctr = nullptr;      // grid-barrier counter of the cooperative vote launches
   DevBuf errs;
   HostBuf hout;                          // pinned result staging
   std::atomic<uint64_t> launches{0};
@@ -420,6 +421,19 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
     p.partials = static_cast<uint32_t*>(ctx->partials.get(bytes));
   }
   dim3 grid((unsigned)per_band, (unsigned)n_bands);
+  // With partials and a grid that is co-resident (one CTA per SM slot), the
+  // kernel reduces the partials itself behind a grid barrier (cooperative
+  // launch guarantees co-residency); larger grids use the reduce kernels.
+  const bool in_kernel_reduce = use_partials && per_band * n_bands <= (long long)ctx->num_sms * bps;
+  if (in_kernel_reduce) {
+    p.sync_ctr = ctx->sync_ctr;
+    ck(cudaMemsetAsync(ctx->sync_ctr, 0, sizeof(unsigned int), s), "memset");
+    void* args[] = {&p};
+    ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), grid, dim3(tfg::kThreads), args, smem, s),
+       "glcm_vote_kernel cooperative launch");
+    ctx->launches++;
+    return;
+  }
   fn<<<grid, tfg::kThreads, smem, s>>>(p);
   ck(cudaGetLastError(), "glcm_vote_kernel launch");
   ctx->launches++;
@@ -672,6 +686,7 @@ int tfg_ctx_create(tfg_ctx** out, int device, unsigned flags) {
     }
     ck(cudaMalloc(&ctx->d_err, 64), "cudaMalloc");
     ck(cudaMemset(ctx->d_err, 0, 64), "memset");
+    ck(cudaMalloc(&ctx->sync_ctr, 64), "cudaMalloc");
   });
   if (rc != TFG_OK) {
     tfg_ctx_destroy(ctx);
@@ -706,6 +721,7 @@ void tfg_ctx_destroy(tfg_ctx* ctx) {
       if (ctx->consumed[i]) cudaEventDestroy(ctx->consumed[i]);
     }
     if (ctx->d_err) cudaFree(ctx->d_err);
+    if (ctx->sync_ctr) cudaFree(ctx->sync_ctr);
     if (ctx->exec) cudaStreamDestroy(ctx->exec);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (prev >= 0) cudaSetDevice(prev);

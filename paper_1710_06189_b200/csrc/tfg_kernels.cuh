@@ -86,6 +86,7 @@ struct VoteParams {
   uint32_t ne_mul, ne_shr;          // fast division by ne
   long long edge_items;             // nrows * ne
   long long edge_per_cta;
+  unsigned int* sync_ctr;           // non-null: cooperative launch, in-kernel partial reduction
 };
 
 // ---------------------------------------------------------------------------
@@ -395,6 +396,78 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t 
 }
 
 // ---------------------------------------------------------------------------
+// Grid-wide barrier for a cooperative (co-resident) launch: every CTA has
+// stored its partial; thread 0 publishes arrival (release) and waits for all
+// `n` CTAs (acquire). The counter is zeroed by the host before the launch.
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int n) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned int v = 0;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= n) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+// After the grid barrier: CTA x of a band sums slice x of the band's
+// gridDim.x partials (read through L2: __ldcg) and adds it to the u64 GLCM.
+// PACKED16 partials are packed u16 pairs (word k = a + 256 b', halves b' and
+// b' + 128; residuals < 2^16 each, so u32 sums cannot overflow); the others
+// are u32 cells (summed in u64).
+template <bool PACKED>
+__device__ __forceinline__ void reduce_partials_slice(const VoteParams& p, uint32_t* scratch, int band_idx,
+                                                      unsigned long long* glcm) {
+  const uint32_t nparts = gridDim.x;
+  const uint32_t L = (uint32_t)p.levels;
+  const uint32_t words = PACKED ? (uint32_t)p.hist_words : L * L;
+  const uint32_t slice = ((words + nparts - 1) / nparts + 3) & ~3u;
+  const uint32_t w0 = min(words, blockIdx.x * slice), w1 = min(words, w0 + slice);
+  if (w0 >= w1) return;
+  const uint32_t* base = p.partials + (size_t)band_idx * nparts * words;
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(scratch);  // [ncol][2]
+  // columns in chunks of at most blockDim.x; thread t: column t % ncol,
+  // partials t / ncol, t / ncol + groups, ...
+  for (uint32_t c0 = w0; c0 < w1; c0 += blockDim.x) {
+    const uint32_t ncol = min((uint32_t)blockDim.x, w1 - c0);
+    const uint32_t groups = blockDim.x / ncol;
+    const uint32_t col = threadIdx.x % ncol, g0 = threadIdx.x / ncol;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 2 * ncol; i += blockDim.x) acc[i] = 0;
+    __syncthreads();
+    if (g0 < groups) {
+      unsigned long long lo = 0, hi = 0;
+      for (uint32_t q = g0; q < nparts; q += groups) {
+        const uint32_t v = __ldcg(base + (size_t)q * words + c0 + col);
+        if (PACKED) {
+          lo += v & 0xFFFFu;
+          hi += v >> 16;
+        } else {
+          lo += v;
+        }
+      }
+      if (lo) atomicAdd(acc + 2 * col, lo);
+      if (hi) atomicAdd(acc + 2 * col + 1, hi);
+    }
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < ncol; c += blockDim.x) {
+      const uint32_t w = c0 + c;
+      if (PACKED) {
+        const uint32_t a = w & 0xFFu, b = w >> 8;
+        if (acc[2 * c]) atomicAdd(glcm + b * L + a, acc[2 * c]);
+        if (acc[2 * c + 1]) atomicAdd(glcm + (b + 128u) * L + a, acc[2 * c + 1]);
+      } else if (acc[2 * c]) {
+        atomicAdd(glcm + w, acc[2 * c]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1 + K2: fused quantise, vote, privatised merge.
 //
 // Two passes over the CTA's share of the anchor raster:
@@ -598,34 +671,43 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   __syncthreads();
 
   // K2 epilogue. PACKED16 with partials: the CTA's packed u16-pair words are
-  // stored as they are (coalesced 16-byte stores, half the bytes of u32 cells)
-  // and unpacked by glcm_reduce_packed_kernel. Otherwise: merge the copies of
-  // each real cell (b, a), then one u64 atomic per cell or one plain store
-  // into this CTA's u32 partial.
-  if constexpr (STRAT == S_PACKED16) {
-    if (p.partials) {
+  // stored as they are (coalesced 16-byte stores, half the bytes of u32 cells).
+  // Otherwise: merge the copies of each real cell (b, a), then one u64 atomic
+  // per cell or one plain store into this CTA's u32 partial. With partials and
+  // a co-resident (cooperative) grid, the CTAs then meet at a grid barrier and
+  // each sums one slice of all its band's partials while they are still in L2
+  // (reduce_partials_slice); otherwise glcm_reduce_*_kernel does it.
+  if (p.partials) {
+    if constexpr (STRAT == S_PACKED16) {
       uint4* dst = reinterpret_cast<uint4*>(p.partials + ((size_t)band_idx * gridDim.x + blockIdx.x) * (size_t)p.hist_words);
       const uint4* src = reinterpret_cast<const uint4*>(hist);
       for (int i = tid; i < (p.hist_words >> 2); i += kThreads) dst[i] = src[i];
-      return;
+    } else {
+      uint32_t* part = p.partials + ((size_t)band_idx * gridDim.x + blockIdx.x) * (size_t)cells;
+      constexpr int RC = strat_copies(STRAT);
+      for (int c = tid; c < cells; c += kThreads) {
+        const uint32_t b = (uint32_t)c / L, a = (uint32_t)c - b * L;
+        const uint32_t pos = cell_pos<STRAT>(b, a);
+        uint32_t sum = 0;
+#pragma unroll 8
+        for (int k = 0; k < RC; ++k) sum += hist[pos * RC + ((k + lane) & (RC - 1))];
+        part[c] = sum;
+      }
     }
+    if (p.sync_ctr) {
+      grid_barrier(p.sync_ctr, gridDim.x * gridDim.y);
+      reduce_partials_slice<STRAT == S_PACKED16>(p, hist, band_idx, glcm);
+    }
+    return;
   }
-  uint32_t* part = p.partials
-                       ? p.partials + ((size_t)band_idx * gridDim.x + blockIdx.x) * (size_t)cells
-                       : nullptr;
   constexpr int RC = strat_copies(STRAT);
   for (int c = tid; c < cells; c += kThreads) {
     const uint32_t b = (uint32_t)c / L, a = (uint32_t)c - b * L;
     const uint32_t pos = cell_pos<STRAT>(b, a);
-    uint32_t s = 0;
-    if constexpr (STRAT == S_PACKED16) {
-      s = (hist[pos & 0x7fffu] >> ((pos >> 11) & 16u)) & 0xFFFFu;
-    } else {
+    uint32_t sum = 0;
 #pragma unroll 8
-      for (int k = 0; k < RC; ++k) s += hist[pos * RC + ((k + lane) & (RC - 1))];
-    }
-    if (part) part[c] = s;
-    else if (s) atomicAdd(glcm + c, (unsigned long long)s);
+    for (int k = 0; k < RC; ++k) sum += hist[pos * RC + ((k + lane) & (RC - 1))];
+    if (sum) atomicAdd(glcm + c, (unsigned long long)sum);
   }
 }
 
