@@ -265,12 +265,15 @@ __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], cons
       }
     }
     if constexpr (STRAT == S_PACKED16) {
+      // reference bytes with the half bit cleared: PRMT then yields the word
+      // index a + 256 (b & 127) directly (no per-vote mask)
       uint32_t flag = 0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t Qm = Q[i] & 0x7F7F7F7Fu;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          flag |= atom_smem(vote_addr<STRAT>(hb, pair_x(P[i], Q[i], j)), packed_inc(Q[i], j));
+        for (int j = 0; j < 4; ++j) flag |= atom_smem(hb + pair_x(P[i], Qm, j) * 4u, packed_inc(Q[i], j));
+      }
       if (flag & kDrainBit)
         packed_drain_item(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], 0xFFFFu, glcm, L);
     } else {
