@@ -136,13 +136,46 @@ def exchange_halo(slab, owned_rows: int, width: int, halo: int, world: int, rank
 
     if halo == 0 or world == 1:
         return owned_rows
+    # gloo moves CPU tensors only: stage a CUDA slab through host memory
+    # (test mode: several ranks sharing one GPU); NCCL moves it in place.
+    stage = slab.is_cuda and dist.get_backend() != "nccl"
     ops = []
     if rank > 0:
-        ops.append(dist.P2POp(dist.isend, slab[: halo * width].contiguous(), rank - 1))
+        send = slab[: halo * width].contiguous()
+        ops.append(dist.P2POp(dist.isend, send.cpu() if stage else send, rank - 1))
     recv = None
     if rank + 1 < world:
-        recv = slab[owned_rows * width:(owned_rows + halo) * width]
+        dst = slab[owned_rows * width:(owned_rows + halo) * width]
+        recv = dst.cpu() if stage else dst
         ops.append(dist.P2POp(dist.irecv, recv, rank + 1))
     for req in dist.batch_isend_irecv(ops):
         req.wait()
+    if stage and recv is not None:
+        dst.copy_(recv)
     return owned_rows + (halo if rank + 1 < world else 0)
+
+
+def reduce_sum_(t, dst: int = 0) -> None:
+    """In-place SUM reduce of `t` to rank `dst` (NCCL on the CUDA tensor;
+    staged through host memory under gloo)."""
+    import torch.distributed as dist
+
+    if t.is_cuda and dist.get_backend() != "nccl":
+        c = t.cpu()
+        dist.reduce(c, dst=dst, op=dist.ReduceOp.SUM)
+        if dist.get_rank() == dst:
+            t.copy_(c)
+        return
+    dist.reduce(t, dst=dst, op=dist.ReduceOp.SUM)
+
+
+def all_reduce_max_(t) -> None:
+    """In-place MAX all-reduce (timing: the slowest rank defines the step)."""
+    import torch.distributed as dist
+
+    if t.is_cuda and dist.get_backend() != "nccl":
+        c = t.cpu()
+        dist.all_reduce(c, op=dist.ReduceOp.MAX)
+        t.copy_(c)
+        return
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
