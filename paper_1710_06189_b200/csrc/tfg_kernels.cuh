@@ -559,31 +559,30 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   const long long mend64 = min(mbeg64 + p.main_per_cta, p.main_items);
   const uint32_t mbeg = (uint32_t)mbeg64;
   const uint32_t m_items = mend64 > mbeg64 ? (uint32_t)(mend64 - mbeg64) : 0u;
-  const uint32_t n_dbl = (m_items + 63) / 64;
   const uint32_t wrap_off = pitch - ni * 16u;  // next row, back to interior segment 0
 
-  // double batch t -> items lane and lane+32 of [mbeg + 64t, +64)
+  // double batch t -> items lane and lane+32 of [mbeg + 64t, +64). Only
+  // whole double batches run here; a CTA's last partial one (< 64 items)
+  // joins the edge pass.
+  const uint32_t n_full_dbl = m_items / 64;
+  const uint32_t lane16 = lane << 4;
   auto issue_dbl = [&](uint32_t t, RawItem& x0, RawItem& x1) {
     const uint32_t f0 = mbeg + t * 64;                       // warp-uniform
     const uint32_t row0 = fast_div(f0, p.ni_mul, p.ni_shr);
     const uint32_t jj0 = f0 - row0 * ni;
     const uint8_t* base = band + (unsigned long long)row0 * pitch + ((p.ch0 + 1 + jj0) << 4);
-    const bool tail = (t + 1) * 64 > m_items;               // warp-uniform
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      RawItem& it = k ? x1 : x0;
-      const uint32_t d = lane + 32u * k;
-      const uint32_t jj = jj0 + d;
-      const uint32_t off = (jj >= ni ? wrap_off : 0u) + (d << 4);  // ni >= 64: at most one wrap
-      const uint8_t* ap = base + off;
-      it.mask = 0xFFFFu;
-      if (tail && t * 64 + d >= m_items) {
-        it.mask = 0;
-        continue;
-      }
-      it.a = ldg16(ap);
-      if constexpr (!ksel_c0_is_anchor<KSEL>()) it.c0 = ldg16(ap + p.ref_off);
-      if constexpr (ksel_needs_c1<KSEL>()) it.c1 = ldg16(ap + p.ref_off + 16);
+    const uint8_t* rbase = base + p.ref_off;
+    const uint32_t off0 = lane16 + (jj0 + lane >= ni ? wrap_off : 0u);  // ni >= 64: at most one wrap
+    const uint32_t off1 = lane16 + 512u + (jj0 + lane + 32u >= ni ? wrap_off : 0u);
+    x0.a = ldg16(base + off0);
+    x1.a = ldg16(base + off1);
+    if constexpr (!ksel_c0_is_anchor<KSEL>()) {
+      x0.c0 = ldg16(rbase + off0);
+      x1.c0 = ldg16(rbase + off1);
+    }
+    if constexpr (ksel_needs_c1<KSEL>()) {
+      x0.c1 = ldg16(rbase + off0 + 16);
+      x1.c1 = ldg16(rbase + off1 + 16);
     }
   };
 
@@ -591,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   // L2 bulk prefetch of the stream's leading edge (reference bytes of double
   // batches [b0, b0 + nb)), issued by the grab that crosses a multiple of kSpan.
   auto prefetch_span = [&](uint32_t b0, uint32_t nbat) {
-    if (b0 >= n_dbl) return;
+    if (b0 >= n_full_dbl) return;
     const uint32_t i0 = mbeg + b0 * 64;
     const uint32_t i1 = mbeg + min(m_items, (b0 + nbat) * 64) - 1;
     const uint32_t r0 = fast_div(i0, p.ni_mul, p.ni_shr), r1 = fast_div(i1, p.ni_mul, p.ni_shr);
@@ -613,44 +612,37 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
 
   RawItem a0, a1, b0i, b1i;
   uint32_t ta = 2 * warp, tb = 2 * warp + 1;
-  if (ta < n_dbl) issue_dbl(ta, a0, a1);
-  if (tb < n_dbl) issue_dbl(tb, b0i, b1i);
+  if (ta < n_full_dbl) issue_dbl(ta, a0, a1);
+  if (tb < n_full_dbl) issue_dbl(tb, b0i, b1i);
   if (tid == 0) {
     s_ticket = 2 * kWarps;
     for (uint32_t q = 0; q < kAhead + kSpan; q += kSpan) prefetch_span(q + 2 * kWarps, kSpan);
   }
   __syncthreads();  // histogram zeroed, ticket counter set
 
-  // Only the CTA's last double batch can be partial (warp-uniform test).
-  const uint32_t n_full_dbl = m_items / 64;
-  auto vote_dbl = [&](uint32_t t, const RawItem& x0, const RawItem& x1) {
-    if (t < n_full_dbl) {
-      vote_full(x0);
-      vote_full(x1);
-    } else {
-      vote_item(x0);
-      vote_item(x1);
-    }
+  auto vote_dbl = [&](uint32_t, const RawItem& x0, const RawItem& x1) {
+    vote_full(x0);
+    vote_full(x1);
   };
   // one ticket grab (4 double batches) per two revolutions of the ring
   for (;;) {
-    if (ta >= n_dbl) break;
+    if (ta >= n_full_dbl) break;
     vote_dbl(ta, a0, a1);
     const uint32_t tn = grab4();
     ta = tn;
-    if (ta < n_dbl) issue_dbl(ta, a0, a1);
-    if (tb >= n_dbl) break;
+    if (ta < n_full_dbl) issue_dbl(ta, a0, a1);
+    if (tb >= n_full_dbl) break;
     vote_dbl(tb, b0i, b1i);
     tb = tn + 1;
-    if (tb < n_dbl) issue_dbl(tb, b0i, b1i);
-    if (ta >= n_dbl) break;
+    if (tb < n_full_dbl) issue_dbl(tb, b0i, b1i);
+    if (ta >= n_full_dbl) break;
     vote_dbl(ta, a0, a1);
     ta = tn + 2;
-    if (ta < n_dbl) issue_dbl(ta, a0, a1);
-    if (tb >= n_dbl) break;
+    if (ta < n_full_dbl) issue_dbl(ta, a0, a1);
+    if (tb >= n_full_dbl) break;
     vote_dbl(tb, b0i, b1i);
     tb = tn + 3;
-    if (tb < n_dbl) issue_dbl(tb, b0i, b1i);
+    if (tb < n_full_dbl) issue_dbl(tb, b0i, b1i);
   }
 
   // ---------------- edge pass: first/last segment of each row (or all) -----
@@ -660,14 +652,23 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     const uint32_t ebeg = (uint32_t)ebeg64;
     const uint32_t e_items = eend64 > ebeg64 ? (uint32_t)(eend64 - ebeg64) : 0u;
     const uint32_t ne = (uint32_t)p.ne;
-    for (uint32_t t = warp; t * 32 < e_items; t += kWarps) {
+    const uint32_t tail0 = mbeg + n_full_dbl * 64, n_tail = m_items - n_full_dbl * 64;  // main-pass leftovers
+    const uint32_t n_work = e_items + n_tail;
+    for (uint32_t t = warp; t * 32 < n_work; t += kWarps) {
       const uint32_t local = t * 32 + lane;
-      const uint32_t e = ebeg + local;
-      const uint32_t row = fast_div(e, p.ne_mul, p.ne_shr);
-      const uint32_t r = e - row * ne;
-      const uint32_t j = ni ? (r ? nch - 1 : 0u) : r;
+      uint32_t row, j;
+      if (local < e_items) {
+        const uint32_t e = ebeg + local;
+        row = fast_div(e, p.ne_mul, p.ne_shr);
+        const uint32_t r = e - row * ne;
+        j = ni ? (r ? nch - 1 : 0u) : r;
+      } else {
+        const uint32_t f = tail0 + (local - e_items);
+        row = fast_div(f, p.ni_mul, p.ni_shr);
+        j = 1 + (f - row * ni);
+      }
       RawItem it;
-      issue_item<KSEL>(p, band, row, j, local < e_items, it);
+      issue_item<KSEL>(p, band, row, j, local < n_work, it);
       vote_item(it);
     }
   }
