@@ -141,12 +141,14 @@ int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height,
  * of which anchors in rows [0, owned_rows) vote; rows [owned_rows,
  * buffer_rows) are the next shard's read-only halo. Host input streams
  * through the Scheme-3 pipeline, device input (TFG_INPUT_DEVICE) votes in
- * place. counts_out: n_dt*L*L u64 partial counts (host) for the caller's
- * reduce (merge_chunk_glcms, pipeline.hpp:231-240, or one NCCL reduce).
+ * place. n_bands images of the same shape may be passed at band_stride bytes
+ * apart (one continuous copy/vote pipeline over all of them).
+ * counts_out: n_bands*n_dt*L*L u64 partial counts (host, band-major) for the
+ * caller's reduce (merge_chunk_glcms, pipeline.hpp:231-240, or one NCCL reduce).
  */
 int tfg_glcm_shard(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t buffer_rows, size_t owned_rows,
-                   size_t pitch, int pixel_levels, int levels, const int* distances, const int* angles_deg,
-                   int n_dt, unsigned flags, uint64_t* counts_out);
+                   size_t pitch, size_t band_stride, size_t n_bands, int pixel_levels, int levels,
+                   const int* distances, const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out);
 
 /*
  * Scheme 3 (compute_glcm_chunked, pipeline.hpp:246-337): K row chunks from

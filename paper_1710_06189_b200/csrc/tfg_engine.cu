@@ -564,8 +564,9 @@ int host_memory_kind(const void* p) {
 
 // Host copy split over up to 8 threads (pageable -> pinned staging).
 void parallel_memcpy(uint8_t* dst, const uint8_t* src, size_t n) {
-  const size_t kMinPerThread = 4u << 20;
-  const size_t nt = std::min<size_t>(8, std::max<size_t>(1, n / kMinPerThread));
+  const size_t kMinPerThread = 2u << 20;
+  const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nt = std::min<size_t>(std::min<size_t>(hw, 16), std::max<size_t>(1, n / kMinPerThread));
   if (nt <= 1) {
     std::memcpy(dst, src, n);
     return;
@@ -581,7 +582,7 @@ void parallel_memcpy(uint8_t* dst, const uint8_t* src, size_t n) {
 
 size_t auto_chunks(size_t width, size_t height, int max_d) {
   const size_t bytes = width * height;
-  const size_t target = 32u << 20;  // ~32 MiB per chunk
+  const size_t target = 32u << 20;  // ~32 MiB per chunk (per-launch overhead vs pipeline fill/drain)
   size_t k = (bytes + target - 1) / target;
   const size_t cap = height / (size_t)(max_d + 1);
   if (k > cap) k = cap;
@@ -623,30 +624,34 @@ std::vector<uint64_t> chunk_specs(size_t width, size_t height, const int* distan
 template <typename Fetch>
 void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, int levels,
                   const int* distances, const int* angles, int n_dt, size_t k, unsigned flags,
-                  unsigned long long* d_acc, Fetch&& fetch_rows, size_t total_rows = 0) {
+                  unsigned long long* d_acc, Fetch&& fetch_rows, size_t total_rows = 0, size_t n_bands = 1,
+                  size_t acc_band_stride = 0) {
+  // The ring runs continuously over (band, chunk): band b+1's first copy
+  // overlaps band b's last votes. Band b's GLCMs go to d_acc + b*acc_band_stride.
   const std::vector<uint64_t> specs = chunk_specs(width, height, distances, angles, n_dt, k, total_rows);
   const size_t pitch = round16(width);
   size_t max_rows = 0;
   for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, specs[3 * i + 2] - specs[3 * i]);
   const bool sequential = (flags & TFG_SEQUENTIAL) != 0;
   for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->dslot[sl].get(max_rows * pitch + 64);
-  for (size_t i = 0; i < k; ++i) {
-    const int sl = (int)(i % tfg_ctx::kSlots);
+  for (size_t n = 0; n < n_bands * k; ++n) {
+    const size_t bnd = n / k, i = n % k;
+    const int sl = (int)(n % tfg_ctx::kSlots);
     const size_t start = specs[3 * i], owned_end = specs[3 * i + 1], buf_end = specs[3 * i + 2];
     const size_t rows = buf_end - start;
     // host side: the slot's previous H2D must be done before we refill it
-    if (i >= (size_t)tfg_ctx::kSlots) ck(cudaEventSynchronize(ctx->copied[sl]), "event sync");
-    const uint8_t* src = fetch_rows(i, start, owned_end, buf_end, sl);
+    if (n >= (size_t)tfg_ctx::kSlots) ck(cudaEventSynchronize(ctx->copied[sl]), "event sync");
+    const uint8_t* src = fetch_rows(bnd, i, start, owned_end, buf_end, sl);
     uint8_t* dst = static_cast<uint8_t*>(ctx->dslot[sl].p);
     // device side: the slot's previous votes must be done before overwrite
-    if (i >= (size_t)tfg_ctx::kSlots) ck(cudaStreamWaitEvent(ctx->copy, ctx->consumed[sl], 0), "wait");
+    if (n >= (size_t)tfg_ctx::kSlots) ck(cudaStreamWaitEvent(ctx->copy, ctx->consumed[sl], 0), "wait");
     ck(cudaMemcpy2DAsync(dst, pitch, src, width, width, rows, cudaMemcpyHostToDevice, ctx->copy), "H2D chunk");
     ck(cudaEventRecord(ctx->copied[sl], ctx->copy), "event record");
     ck(cudaStreamWaitEvent(ctx->exec, ctx->copied[sl], 0), "wait");
     if (pixel_levels == levels) launch_validate(ctx, dst, width, rows, pitch, 0, 1, levels, ctx->d_err, ctx->exec);
     for (int t = 0; t < n_dt; ++t)
       launch_vote(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, levels, distances[t],
-                  angles[t], flags, d_acc + (size_t)t * levels * levels, ctx->exec);
+                  angles[t], flags, d_acc + bnd * acc_band_stride + (size_t)t * levels * levels, ctx->exec);
     ck(cudaEventRecord(ctx->consumed[sl], ctx->exec), "event record");
     if (sequential) ck(cudaStreamSynchronize(ctx->exec), "stream sync");
   }
@@ -850,12 +855,12 @@ int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size
     ck(cudaMemsetAsync(d_acc, 0, n_out * cells * 8, s), "memset");
     const bool dev = (flags & TFG_INPUT_DEVICE) != 0;
 
-    if (!dev && n_bands == 1) {
-      // host image -> Scheme-3 stream pipeline (copy chunk i+1 while voting chunk i)
+    if (!dev) {
+      // host image(s) -> Scheme-3 stream pipeline over (band, chunk): copy
+      // chunk n+1 while voting chunk n, across band boundaries
       int dmax = 1;
       for (int i = 0; i < n_dt; ++i) dmax = std::max(dmax, distances[i]);
       const size_t k = auto_chunks(width, owned_rows, dmax);
-      // per-(d,theta) accumulators are contiguous: d_acc + t*cells
       if (pitch != width) fail(TFG_INVALID_ARGUMENT, "glcm: host images must be dense (pitch == width)");
       // Pinned caller memory is DMA'd in place. Pageable memory would make
       // every cudaMemcpyAsync a synchronous bounce-buffer copy, so its rows are
@@ -869,13 +874,14 @@ int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size
       }
       run_pipeline(
           ctx, width, owned_rows, pixel_levels, levels, distances, angles_deg, n_dt, k, flags, d_acc,
-          [&](size_t, size_t start, size_t, size_t buf_end, int sl) -> const uint8_t* {
-            if (!pageable) return px + start * width;
+          [&](size_t b, size_t, size_t start, size_t, size_t buf_end, int sl) -> const uint8_t* {
+            const uint8_t* src = px + b * band_stride + start * width;
+            if (!pageable) return src;
             uint8_t* dst = static_cast<uint8_t*>(ctx->hslot[sl].p);
-            parallel_memcpy(dst, px + start * width, (buf_end - start) * width);
+            parallel_memcpy(dst, src, (buf_end - start) * width);
             return dst;
           },
-          height);
+          height, n_bands, (size_t)n_dt * cells);
       if (pixel_levels == levels) check_async_flag(ctx, s);
       finish(ctx, d_acc, (int)n_out, levels, flags, counts_out, probs_out, feats_out, s);
       return;
@@ -931,11 +937,11 @@ int tfg_glcm_bands(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height,
 }
 
 int tfg_glcm_shard(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t buffer_rows, size_t owned_rows,
-                   size_t pitch, int pixel_levels, int levels, const int* distances, const int* angles_deg, int n_dt,
-                   unsigned flags, uint64_t* counts_out) {
-  return glcm_impl(ctx, px, width, buffer_rows, owned_rows, pitch, pitch * buffer_rows, 1, pixel_levels, levels,
-                   distances, angles_deg, n_dt, flags & ~(TFG_SYMMETRIC | TFG_NORMALIZE | TFG_FEATURES), counts_out,
-                   nullptr, nullptr);
+                   size_t pitch, size_t band_stride, size_t n_bands, int pixel_levels, int levels,
+                   const int* distances, const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out) {
+  return glcm_impl(ctx, px, width, buffer_rows, owned_rows, pitch, n_bands > 1 ? band_stride : pitch * buffer_rows,
+                   n_bands, pixel_levels, levels, distances, angles_deg, n_dt,
+                   flags & ~(TFG_SYMMETRIC | TFG_NORMALIZE | TFG_FEATURES), counts_out, nullptr, nullptr);
 }
 
 int tfg_glcm(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t pitch, int pixel_levels,
@@ -967,7 +973,7 @@ int tfg_glcm_chunked(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels
     for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->hslot[sl].get(max_rows * width + 64);
     try {
       run_pipeline(ctx, width, height, pixel_levels, levels, distances, angles_deg, n_dt, chunk_count, flags, d_acc,
-                   [&](size_t i, size_t start, size_t owned_end, size_t buf_end, int sl) -> const uint8_t* {
+                   [&](size_t, size_t i, size_t start, size_t owned_end, size_t buf_end, int sl) -> const uint8_t* {
                      uint8_t* dst = static_cast<uint8_t*>(ctx->hslot[sl].p);
                      char msg[512] = {0};
                      const int rc = fetch(user, i, start, owned_end, buf_end, dst, msg, sizeof msg);

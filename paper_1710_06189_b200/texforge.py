@@ -301,25 +301,29 @@ class Engine:
         return out[0] if len(out) == 1 else tuple(out)
 
     def shard(self, pixels, width: int, buffer_rows: int, owned_rows: int, levels: int,
-              dts: Sequence[Tuple[int, int]], pixel_levels: int = 256, device: bool = False) -> np.ndarray:
-        """Partial counts [n_dt, L, L] of one row shard (tfg_glcm_shard): anchors in
-        rows [0, owned_rows) of a buffer of `buffer_rows` rows vote; the rest is
-        the next shard's halo. `pixels` is host memory (numpy) or, with
-        device=True, a device address (int) of a 16-byte-aligned dense buffer."""
+              dts: Sequence[Tuple[int, int]], pixel_levels: int = 256, device: bool = False,
+              n_bands: int = 1, band_stride: int = 0) -> np.ndarray:
+        """Partial counts [n_bands, n_dt, L, L] of row shards (tfg_glcm_shard):
+        anchors in rows [0, owned_rows) of a buffer of `buffer_rows` rows vote;
+        the rest is the next shard's halo. n_bands buffers of that shape sit
+        `band_stride` bytes apart (default: dense). `pixels` is host memory
+        (numpy) or, with device=True, a device address (int) of a
+        16-byte-aligned dense buffer."""
         n_dt = len(dts)
         d = (C.c_int * n_dt)(*[int(x[0]) for x in dts])
         a = (C.c_int * n_dt)(*[int(x[1]) for x in dts])
-        counts = np.zeros(n_dt * levels * levels, dtype=np.uint64)
+        counts = np.zeros(n_bands * n_dt * levels * levels, dtype=np.uint64)
+        stride = band_stride or width * buffer_rows
         if device:
             ptr, flags = C.c_void_p(int(pixels)), L.TFG_INPUT_DEVICE
         else:
             px = np.ascontiguousarray(pixels, dtype=np.uint8).reshape(-1)
-            if px.size < width * buffer_rows:
+            if px.size < stride * (n_bands - 1) + width * buffer_rows:
                 raise ValueError("glcm: pixel count does not match dimensions")
             ptr, flags = px.ctypes.data_as(C.c_void_p), 0
-        L.check(self._lib.tfg_glcm_shard(self.handle, ptr, width, buffer_rows, owned_rows, width, pixel_levels,
-                                         levels, d, a, n_dt, flags, _ptr(counts, C.c_uint64)))
-        return counts.reshape(n_dt, levels, levels)
+        L.check(self._lib.tfg_glcm_shard(self.handle, ptr, width, buffer_rows, owned_rows, width, stride, n_bands,
+                                         pixel_levels, levels, d, a, n_dt, flags, _ptr(counts, C.c_uint64)))
+        return counts.reshape(n_bands, n_dt, levels, levels)
 
     def chunked(self, source: ChunkSource, dts: Sequence[Tuple[int, int]], chunk_count: int,
                 pixel_levels: int, levels: int, flags: int = 0) -> np.ndarray:
