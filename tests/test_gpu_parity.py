@@ -268,3 +268,56 @@ def test_async_device_shards_sum_to_whole(engine):
         got = acc.cpu().numpy().view(np.uint64)
         assert np.array_equal(got, O.glcm_gray(gray, w, h, levels, d, a)), (d, a)
     L.check(lib.tfg_check_async_errors(engine.handle))
+
+
+def _oracle_rows(gray, w, rows, levels, d, a, owned):
+    q = O.quantize(gray, levels)
+    return O.glcm_rows(q, w, rows, levels, d, a, 0, owned)
+
+
+def test_shard_bands_host_pipeline(engine):
+    # row shards of two images through one continuous host pipeline: owned
+    # rows vote, the halo rows below them are read-only (tfg_glcm_shard)
+    w, rows, owned = 2048, 9000, 8997
+    imgs = [tf.synth_noise(w, rows, 11).pixels, tf.synth_smooth(w, rows, 12).pixels]
+    dts = [(1, 0), (3, 45), (2, 90), (1, 135)]
+    got = engine.shard(np.concatenate(imgs), w, rows, owned, 256, dts, n_bands=2)
+    for b in range(2):
+        for t, (d, a) in enumerate(dts):
+            assert np.array_equal(got[b, t].reshape(-1), _oracle_rows(imgs[b], w, rows, 256, d, a, owned)), (b, d, a)
+
+
+def test_shard_device_input(engine):
+    import torch
+    w, rows, owned = 1040, 700, 650
+    gray = tf.synth_noise(w, rows, 13).pixels
+    dev = torch.from_numpy(gray).cuda()
+    dts = [(1, 0), (4, 135)]
+    for levels in (32, 256):
+        got = engine.shard(dev.data_ptr(), w, rows, owned, levels, dts, device=True)
+        for t, (d, a) in enumerate(dts):
+            assert np.array_equal(got[0, t].reshape(-1), _oracle_rows(gray, w, rows, levels, d, a, owned))
+
+
+def test_pinned_host_input(engine):
+    import torch
+    w, h = 4096, 3000
+    gray = tf.synth_smooth(w, h, 3).pixels
+    pinned = torch.from_numpy(gray).pin_memory()
+    assert engine._lib.tfg_memory_kind(C.c_void_p(pinned.data_ptr())) == 1
+    dts = [(1, 0), (2, 90)]
+    got = engine.glcm(pinned.numpy(), w, h, 256, dts)
+    for t, (d, a) in enumerate(dts):
+        assert np.array_equal(got[0, t].reshape(-1), O.glcm_gray(gray, w, h, 256, d, a))
+
+
+@pytest.mark.parametrize("levels,nb", [(256, 2), (256, 300), (100, 300)])
+def test_partials_reduce_paths(engine, levels, nb):
+    # L > 64 keeps per-CTA partials: a co-resident grid reduces them in-kernel
+    # behind a grid barrier (cooperative launch); 300 bands exceed one CTA per
+    # SM and take the separate reduce kernels
+    w, h = 160, 40
+    imgs = [tf.synth_noise(w, h, 100 + b).pixels for b in range(nb)]
+    got = engine.glcm(np.concatenate(imgs), w, h, levels, [(1, 45)], n_bands=nb)
+    for b in range(0, nb, max(1, nb // 7)):
+        assert np.array_equal(got[b, 0].reshape(-1), O.glcm_gray(imgs[b], w, h, levels, 1, 45)), b
