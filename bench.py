@@ -558,20 +558,25 @@ def run_engine(args, wl):
             h2d_gbs.append(probe.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9)
         del probe
         red = torch.zeros(o, dtype=torch.int64, device="cuda") if dist else None
+        # results land by DMA in a pinned output buffer, one slice per call
+        out_host = torch.zeros(o, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
 
         def e2e_step():
-            parts = []
+            off = 0
             for L in plan.levels_list:
                 dts = plan.dts
                 if plan.layout == "bands":
                     for kind in kinds:
-                        parts.append(eng.glcm(pinned[kind].numpy(), W, plan.height, L, dts, n_bands=plan.bands)
-                                     .transpose(1, 0, 2, 3).reshape(-1))
+                        n = plan.bands * len(dts) * L * L
+                        eng.glcm(pinned[kind].numpy(), W, plan.height, L, dts, n_bands=plan.bands,
+                                 out=out_host[off:off + n])
+                        off += n
                 else:
-                    c = eng.shard(pinned["all"].numpy(), W, rows_e2e, plan.owned, L, dts, n_bands=len(kinds),
-                                  band_stride=rows_e2e * W)
-                    parts.append(c.reshape(-1))
-            host = np.concatenate(parts)
+                    n = len(kinds) * len(dts) * L * L
+                    eng.shard(pinned["all"].numpy(), W, rows_e2e, plan.owned, L, dts, n_bands=len(kinds),
+                              band_stride=rows_e2e * W, out=out_host[off:off + n])
+                    off += n
+            host = out_host
             if dist is not None and plan.layout.startswith("rows"):
                 red.copy_(torch.from_numpy(host.view(np.int64)))
                 D.reduce_sum_(red)

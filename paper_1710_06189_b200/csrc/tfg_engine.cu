@@ -485,6 +485,21 @@ void check_pixel_levels(int pixel_levels, int levels) {
     fail(TFG_INVALID_ARGUMENT, "glcm: image levels do not match params levels");
 }
 
+// 0 pageable host, 1 pinned host, 2 device, 3 managed (cudaPointerGetAttributes).
+int host_memory_kind(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  switch (a.type) {
+    case cudaMemoryTypeHost: return 1;
+    case cudaMemoryTypeDevice: return 2;
+    case cudaMemoryTypeManaged: return 3;
+    default: return 0;
+  }
+}
+
 // Post-processing of n GLCMs resident at d_counts; results to host buffers.
 void finish(tfg_ctx* ctx, unsigned long long* d_counts, int n, int levels, unsigned flags,
             uint64_t* counts_out, double* probs_out, double* feats_out, cudaStream_t s) {
@@ -519,7 +534,11 @@ void finish(tfg_ctx* ctx, unsigned long long* d_counts, int n, int levels, unsig
   const size_t b_counts = n * cells * 8, b_probs = want_probs ? n * cells * 8 : 0;
   const size_t b_feats = d_feats ? n * 5 * 8 : 0, b_err = want_probs ? 2 * n * sizeof(int) : 0;
   char* h = static_cast<char*>(ctx->hout.get(b_counts + b_probs + b_feats + b_err + 64));
-  ck(cudaMemcpyAsync(h, d_final, b_counts, cudaMemcpyDeviceToHost, s), "D2H counts");
+  // a pinned caller buffer receives the counts by DMA directly (no staging copy)
+  const bool counts_direct = counts_out && host_memory_kind(counts_out) == 1;
+  ck(cudaMemcpyAsync(counts_direct ? static_cast<void*>(counts_out) : static_cast<void*>(h), d_final, b_counts,
+                     cudaMemcpyDeviceToHost, s),
+     "D2H counts");
   if (b_probs) ck(cudaMemcpyAsync(h + b_counts, d_probs, b_probs, cudaMemcpyDeviceToHost, s), "D2H probs");
   if (b_feats) ck(cudaMemcpyAsync(h + b_counts + b_probs, d_feats, b_feats, cudaMemcpyDeviceToHost, s), "D2H feats");
   if (b_err) ck(cudaMemcpyAsync(h + b_counts + b_probs + b_feats, d_errs, b_err, cudaMemcpyDeviceToHost, s), "D2H err");
@@ -532,7 +551,7 @@ void finish(tfg_ctx* ctx, unsigned long long* d_counts, int n, int levels, unsig
       for (int i = 0; i < n; ++i)
         if (e[n + i]) fail(TFG_INVALID_ARGUMENT, "extract_features: input is not normalized");
   }
-  if (counts_out) std::memcpy(counts_out, h, b_counts);
+  if (counts_out && !counts_direct) std::memcpy(counts_out, h, b_counts);
   if (probs_out && b_probs) std::memcpy(probs_out, h + b_counts, b_probs);
   if (feats_out && b_feats) std::memcpy(feats_out, h + b_counts + b_probs, b_feats);
 }
@@ -547,22 +566,7 @@ void check_async_flag(tfg_ctx* ctx, cudaStream_t s) {
   }
 }
 
-// 0 pageable host, 1 pinned host, 2 device, 3 managed (cudaPointerGetAttributes).
-int host_memory_kind(const void* p) {
-  cudaPointerAttributes a{};
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  switch (a.type) {
-    case cudaMemoryTypeHost: return 1;
-    case cudaMemoryTypeDevice: return 2;
-    case cudaMemoryTypeManaged: return 3;
-    default: return 0;
-  }
-}
-
-// Host copy split over up to 8 threads (pageable -> pinned staging).
+// Host copy split over up to 16 host threads (pageable -> pinned staging).
 void parallel_memcpy(uint8_t* dst, const uint8_t* src, size_t n) {
   const size_t kMinPerThread = 2u << 20;
   const size_t hw = std::max(1u, std::thread::hardware_concurrency());

@@ -238,6 +238,14 @@ class MemoryChunkSource(ChunkSource):
 
 
 # --------------------------------------------------------------------------- engine
+def _out_buffer(out: Optional[np.ndarray], n: int) -> np.ndarray:
+    if out is None:
+        return np.zeros(n, dtype=np.uint64)
+    if out.dtype != np.uint64 or out.size != n or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a contiguous uint64 array of {n} elements")
+    return out.reshape(-1)
+
+
 def _ptr(a: np.ndarray, t=C.c_uint8):
     return a.ctypes.data_as(C.POINTER(t))
 
@@ -270,8 +278,10 @@ class Engine:
     # -- raw, multi-(d, theta) entry point -------------------------------------
     def glcm(self, pixels: np.ndarray, width: int, height: int, levels: int, dts: Sequence[Tuple[int, int]],
              pixel_levels: int = 256, flags: int = 0, n_bands: int = 1,
-             want_probs: bool = False, want_features: bool = False):
-        """counts[n_bands, n_dt, L, L] (+ probs, features) of host pixels."""
+             want_probs: bool = False, want_features: bool = False, out: Optional[np.ndarray] = None):
+        """counts[n_bands, n_dt, L, L] (+ probs, features) of host pixels. `out`
+        (u64, n_bands*n_dt*L*L) receives the counts; pinned memory gets them by
+        DMA with no staging copy."""
         px = np.ascontiguousarray(pixels, dtype=np.uint8).reshape(-1)
         if px.size != width * height * n_bands:
             raise ValueError("glcm: pixel count does not match dimensions")
@@ -279,7 +289,7 @@ class Engine:
         d = (C.c_int * n_dt)(*[int(x[0]) for x in dts])
         a = (C.c_int * n_dt)(*[int(x[1]) for x in dts])
         cells = levels * levels
-        counts = np.zeros(n_bands * n_dt * cells, dtype=np.uint64)
+        counts = _out_buffer(out, n_bands * n_dt * cells)
         probs = np.zeros(n_bands * n_dt * cells, dtype=np.float64) if (want_probs or want_features) else None
         feats = np.zeros(n_bands * n_dt * 5, dtype=np.float64) if want_features else None
         if want_probs or want_features:
@@ -302,7 +312,7 @@ class Engine:
 
     def shard(self, pixels, width: int, buffer_rows: int, owned_rows: int, levels: int,
               dts: Sequence[Tuple[int, int]], pixel_levels: int = 256, device: bool = False,
-              n_bands: int = 1, band_stride: int = 0) -> np.ndarray:
+              n_bands: int = 1, band_stride: int = 0, out: Optional[np.ndarray] = None) -> np.ndarray:
         """Partial counts [n_bands, n_dt, L, L] of row shards (tfg_glcm_shard):
         anchors in rows [0, owned_rows) of a buffer of `buffer_rows` rows vote;
         the rest is the next shard's halo. n_bands buffers of that shape sit
@@ -312,7 +322,7 @@ class Engine:
         n_dt = len(dts)
         d = (C.c_int * n_dt)(*[int(x[0]) for x in dts])
         a = (C.c_int * n_dt)(*[int(x[1]) for x in dts])
-        counts = np.zeros(n_bands * n_dt * levels * levels, dtype=np.uint64)
+        counts = _out_buffer(out, n_bands * n_dt * levels * levels)
         stride = band_stride or width * buffer_rows
         if device:
             ptr, flags = C.c_void_p(int(pixels)), L.TFG_INPUT_DEVICE
