@@ -566,23 +566,28 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   // joins the edge pass.
   const uint32_t n_full_dbl = m_items / 64;
   const uint32_t lane16 = lane << 4;
+  // 64-bit bases are formed once; per double batch one row offset, per item
+  // one 32-bit lane offset
+  const uint8_t* const abase0 = band + ((p.ch0 + 1) << 4);
+  const uint8_t* const rbase0 = abase0 + p.ref_off;
   auto issue_dbl = [&](uint32_t t, RawItem& x0, RawItem& x1) {
     const uint32_t f0 = mbeg + t * 64;                       // warp-uniform
     const uint32_t row0 = fast_div(f0, p.ni_mul, p.ni_shr);
     const uint32_t jj0 = f0 - row0 * ni;
-    const uint8_t* base = band + (unsigned long long)row0 * pitch + ((p.ch0 + 1 + jj0) << 4);
-    const uint8_t* rbase = base + p.ref_off;
+    const unsigned long long roff = (unsigned long long)row0 * pitch + (jj0 << 4);
     const uint32_t off0 = lane16 + (jj0 + lane >= ni ? wrap_off : 0u);  // ni >= 64: at most one wrap
     const uint32_t off1 = lane16 + 512u + (jj0 + lane + 32u >= ni ? wrap_off : 0u);
-    x0.a = ldg16(base + off0);
-    x1.a = ldg16(base + off1);
+    const uint8_t* a = abase0 + roff;
+    x0.a = ldg16(a + off0);
+    x1.a = ldg16(a + off1);
+    const uint8_t* r = rbase0 + roff;
     if constexpr (!ksel_c0_is_anchor<KSEL>()) {
-      x0.c0 = ldg16(rbase + off0);
-      x1.c0 = ldg16(rbase + off1);
+      x0.c0 = ldg16(r + off0);
+      x1.c0 = ldg16(r + off1);
     }
     if constexpr (ksel_needs_c1<KSEL>()) {
-      x0.c1 = ldg16(rbase + off0 + 16);
-      x1.c1 = ldg16(rbase + off1 + 16);
+      x0.c1 = ldg16(r + off0 + 16);
+      x1.c1 = ldg16(r + off1 + 16);
     }
   };
 
