@@ -29,7 +29,7 @@
 
 namespace tfg {
 
-constexpr int kThreads = 768;  // threads per vote CTA (24 warps: 85 regs for the 3-slot ring)
+constexpr int kThreads = 1024;  // threads per vote CTA (32 warps)
 
 enum Quant : int {
   Q_NONE = 0,   // values used as-is (gray with L=256, or quantised with L=256)
@@ -188,7 +188,7 @@ __device__ __forceinline__ uint32_t packed_inc(uint32_t Q, int j) {
 // threads drain the same word. Bound: once a field passes 2^15, every warp
 // that votes on it sees bit 15 and drains before its next item, and a warp
 // adds <= 512 to one field per item (32 lanes x 16), so before the first
-// drain lands the field stays < 2^15 + 24 * 512 + 512 < 2^16.
+// drain lands the field stays < 2^15 + 32 * 512 + 512 < 2^16.
 constexpr uint32_t kDrainBit = 0x80008000u;
 static_assert(32768u + (kThreads / 32 + 1) * 512u < 65536u, "PACKED16 field bound");
 
