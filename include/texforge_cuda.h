@@ -200,6 +200,16 @@ int tfg_glcm_bands_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
                          size_t band_stride, size_t n_bands, int pixel_levels, int levels, int distance,
                          int angle_deg, unsigned flags, uint64_t* d_counts, void* stream);
 
+/* Every (d, theta) of a device image (or band batch) in one call: ADDS the
+ * GLCMs into d_counts laid out [n_dt][n_bands][L*L]; anchors in rows
+ * [0, row_end) vote (row_end = height for whole images). One validation pass,
+ * n_dt vote launches enqueued back to back on `stream` (no host round trip
+ * per GLCM). Same stream rule as tfg_glcm_async. */
+int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t height, size_t pitch,
+                         size_t band_stride, size_t n_bands, size_t row_end, int pixel_levels, int levels,
+                         const int* distances, const int* angles_deg, int n_dt, unsigned flags, uint64_t* d_counts,
+                         void* stream);
+
 /* Device post-processing on `stream`: symmetrize (in place allowed? no: out != in). */
 int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned flags,
                    uint64_t* d_sym_out, double* d_probs_out, double* d_feats_out, void* stream);

@@ -1185,6 +1185,37 @@ int tfg_glcm_bands_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
   });
 }
 
+int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t height, size_t pitch,
+                         size_t band_stride, size_t n_bands, size_t row_end, int pixel_levels, int levels,
+                         const int* distances, const int* angles_deg, int n_dt, unsigned flags, uint64_t* d_counts,
+                         void* stream) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  return guarded([&] {
+    check_levels(levels, "glcm");
+    check_pixel_levels(pixel_levels, levels);
+    if (n_dt < 1 || !distances || !angles_deg) fail(TFG_INVALID_ARGUMENT, "glcm: need at least one (distance, angle)");
+    for (int t = 0; t < n_dt; ++t) {
+      check_angle(angles_deg[t]);
+      if (distances[t] < 1 || (size_t)distances[t] >= width)
+        fail(TFG_INVALID_ARGUMENT, "glcm: degenerate geometry (d must be in [1, min(width, height)))");
+    }
+    if ((reinterpret_cast<uintptr_t>(d_px) & 15) || (pitch % 16) || pitch < width || (n_bands > 1 && band_stride % 16))
+      fail(TFG_INVALID_ARGUMENT, "glcm_async: device image must be 16-byte aligned with pitch % 16 == 0");
+    if (n_bands < 1 || n_bands > 65535) fail(TFG_INVALID_ARGUMENT, "glcm: band count must be in [1, 65535]");
+    if (n_bands > 1 && band_stride < pitch * height) fail(TFG_INVALID_ARGUMENT, "glcm: bands overlap");
+    if (row_end > height) fail(TFG_INVALID_ARGUMENT, "glcm_async: row_end > height");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (pixel_levels == levels)
+      launch_validate(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, levels, ctx->d_err, s);
+    const size_t per_dt = n_bands * (size_t)levels * levels;
+    for (int t = 0; t < n_dt; ++t)
+      launch_vote(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, row_end, pixel_levels, levels,
+                  distances[t], angles_deg[t], flags,
+                  reinterpret_cast<unsigned long long*>(d_counts) + (size_t)t * per_dt, s);
+  });
+}
+
 int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned flags, uint64_t* d_sym_out,
                    double* d_probs_out, double* d_feats_out, void* stream) {
   if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
