@@ -407,7 +407,12 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   const int bps = occupancy_for(fn, smem);
   // persistent-style grid: at most one wave of CTAs per band set, and no CTA
   // with less than one round of work.
-  long long per_band = std::max<long long>(1, (long long)ctx->num_sms * bps / std::max(n_bands, 1));
+  // One wave of persistent CTAs when the bands fit in it; otherwise ~8 waves,
+  // so the last, partial wave costs <= ~1/16 of the time (256 bands on 148
+  // SMs at one CTA per band would leave the second wave 27% idle).
+  const long long slots = (long long)ctx->num_sms * bps;
+  long long per_band = n_bands < slots ? std::max<long long>(1, slots / std::max(n_bands, 1))
+                                       : std::max<long long>(1, (8 * slots + n_bands - 1) / n_bands);
   per_band = std::min<long long>(per_band, (p.items + 2 * tfg::kThreads - 1) / (2 * tfg::kThreads));
   per_band = std::max<long long>(per_band, 1);
   p.items_per_cta = (p.items + per_band - 1) / per_band;
