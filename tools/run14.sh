@@ -4,6 +4,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,power.limit --f
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
 for b in dropin_tests refsuite_unit refsuite_accept; do timeout 900 tests/cpp/_build/$b > $O/cpp_$b.log 2>&1; echo "rc=$?" >> $O/cpp_$b.log; done
+TEXFORGE_CLI=$PWD/cli/_build/texforge timeout 900 cli/_build/refsuite_cli > $O/cli_refsuite.log 2>&1; echo "rc=$?" >> $O/cli_refsuite.log
 timeout 900 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err
 timeout 600 python bench.py --impl reference > $O/bench_ref_c3.json 2> $O/bench_ref_c3.err
 for wl in c2 c4 c5 c1; do timeout 900 python bench.py --workload $wl --steps 10 --warmup 3 --cpu-seconds 5 > $O/bench_$wl.json 2> $O/bench_$wl.err; done
