@@ -321,3 +321,17 @@ def test_partials_reduce_paths(engine, levels, nb):
     got = engine.glcm(np.concatenate(imgs), w, h, levels, [(1, 45)], n_bands=nb)
     for b in range(0, nb, max(1, nb // 7)):
         assert np.array_equal(got[b, 0].reshape(-1), O.glcm_gray(imgs[b], w, h, levels, 1, 45)), b
+
+
+@pytest.mark.parametrize("w", [1024, 1040, 1041, 1056, 1057, 1071, 2047, 3001])
+def test_two_pass_split_boundaries(engine, w):
+    # widths around the main/edge split (nch >= 66 -> interior double batches
+    # with row wraps; nch < 66 -> everything in the edge pass), odd widths,
+    # heights that leave < 64 leftover interior items per CTA
+    h = 67
+    gray = tf.synth_noise(w, h, w).pixels
+    dts = [(1, 0), (3, 45), (2, 90), (5, 135), (17, 0), (16, 45)]
+    for levels in (32, 256):
+        got = engine.glcm(gray, w, h, levels, dts)
+        for t, (d, a) in enumerate(dts):
+            assert np.array_equal(got[0, t].reshape(-1), O.glcm_gray(gray, w, h, levels, d, a)), (w, levels, d, a)
