@@ -415,7 +415,6 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
                                        : std::max<long long>(1, (8 * slots + n_bands - 1) / n_bands);
   per_band = std::min<long long>(per_band, (p.items + 2 * tfg::kThreads - 1) / (2 * tfg::kThreads));
   per_band = std::max<long long>(per_band, 1);
-  p.items_per_cta = (p.items + per_band - 1) / per_band;
   p.main_per_cta = ((p.main_items + per_band - 1) / per_band + 63) / 64 * 64;
   p.edge_per_cta = (p.edge_items + per_band - 1) / per_band;
   const bool use_partials = cells > 4096;

@@ -11,18 +11,20 @@
 // K3 symmetrize / normalize, K4 features — post-processing on device.
 //
 // Work decomposition: the valid-anchor raster is cut into
-// 16-pixel "items" (one 16-byte vector per row segment). A warp takes batches
-// of 32 consecutive items (one per lane: every LDG.128 of the warp is one
-// coalesced 512-byte access) from a per-CTA ticket counter and keeps three
-// batches in a register ring (two in flight while one votes). The reference
-// neighbour of each segment is two aligned 16-byte loads + funnel shifts
-// (displacement dcol = 16q + 4k + s: q and the word shift k are launch /
-// template constants, s is a byte funnel shift).
+// 16-pixel "items" (one 16-byte vector per row segment). A main pass votes the
+// interior segments of every row in double batches of 64 consecutive items
+// (lanes l and l+32; every LDG.128 of the warp is one coalesced 512-byte
+// access) taken from a per-CTA ticket counter, two double batches in a
+// register ring; an edge pass votes the row ends with masks. The reference
+// neighbour of each segment is one or two aligned 16-byte loads + funnel
+// shifts (displacement dcol = 16q + 4k + s: q and the word shift k are launch
+// / template constants, s is a byte funnel shift).
 //
-// The vote itself is 3 instructions: the quantised anchor and reference bytes
-// are pre-scaled so that ONE byte permute (PRMT) of an anchor word and a
-// reference word gives a pixel pair's shared-memory offset, then one IMAD adds
-// the lane's copy base and one red.shared.add casts the vote.
+// The vote itself is 3 instructions for L <= 128: the quantised anchor and
+// reference bytes are pre-scaled so that ONE byte permute (PRMT) of an anchor
+// word and a reference word gives a pixel pair's shared-memory offset, then
+// one IMAD adds the lane's copy base and one red.shared.add (ATOMS.POPC.INC)
+// casts the vote; 6 for the packed-u16 L=256 layout (kDrainBit).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -67,7 +69,6 @@ struct VoteParams {
   int ch0, nch;                     // first 16-px chunk, chunks per row
   int nrows;                        // anchor rows [0, nrows)
   long long items;                  // nrows*nch (per band)
-  long long items_per_cta;
   uint32_t div_mul, div_shr;        // fast division by nch (div_mul == 0: nch == 1)
   uint32_t qmask;                   // Q_SHIFT / Q_CLAMP per-byte mask (L-1)*0x01010101
   int qshift;                       // Q_SHIFT: s = 8 - log2 L
