@@ -516,13 +516,54 @@ def compute_glcm_shared(img: QuantizedImage, p: GlcmParams, plan_: ExecutionPlan
     return g, stats_from_counts(g)
 
 
-def compute_glcm_privatized(img: QuantizedImage, p: GlcmParams, plan_: ExecutionPlan,
-                            group_count: int = 0) -> Tuple[Glcm, ContentionStats]:
-    """parallel.hpp:240-254 — Scheme 2: privatised shared-memory sub-GLCMs."""
+def _resolve_group_count(requested: int, plan_: ExecutionPlan, width: int, rows: int) -> int:
+    """parallel.hpp:166-181: 0 -> groups_per_unit * worker_count, raised so no
+    group can exceed 2^32 votes, clamped to [1, rows]."""
+    g = int(requested)
+    if g == 0:
+        g = (plan_.groups_per_unit or 2) * plan_.worker_count
+        floor_groups = -(-(rows * width) // (1 << 32))
+        g = max(g, floor_groups)
+    return max(1, min(g, rows))
+
+
+def _subglcms(img: QuantizedImage, p: GlcmParams, plan_: ExecutionPlan, group_count: int, want_subs: bool):
+    _check_inputs(img, p)
     if plan_.copies < 1:
         raise ValueError("privatized: plan.copies must be >= 1")
-    g = _device_glcm(img, p)
-    return g, stats_from_counts(g)
+    groups = _resolve_group_count(group_count, plan_, img.width, img.height)
+    cells = p.levels * p.levels
+    n_subs = groups * plan_.copies
+    subs = np.zeros(n_subs * cells, dtype=np.uint32) if want_subs else None
+    counts = np.zeros(cells, dtype=np.uint64)
+    hottest = np.zeros(n_subs, dtype=np.uint64)
+    eng = default_engine()
+    px = np.ascontiguousarray(img.pixels, dtype=np.uint8).reshape(-1)
+    L.check(eng._lib.tfg_subglcms(eng.handle, px.ctypes.data_as(C.c_void_p), img.width, img.height, img.levels,
+                                  p.levels, p.distance, int(p.angle), plan_.group_size, plan_.copies, groups, 0,
+                                  subs.ctypes.data_as(C.POINTER(C.c_uint32)) if want_subs else None,
+                                  _ptr(counts, C.c_uint64), _ptr(hottest, C.c_uint64)))
+    return subs, counts, hottest, n_subs
+
+
+def compute_subglcms(img: QuantizedImage, p: GlcmParams, plan_: ExecutionPlan,
+                     group_count: int = 0) -> List[np.ndarray]:
+    """parallel.hpp:218-225 — the raw (group, copy) sub-GLCMs, group-major, with
+    the reference's exact lane -> copy routing (glcm_subglcm_kernel)."""
+    subs, _, _, n_subs = _subglcms(img, p, plan_, group_count, True)
+    cells = p.levels * p.levels
+    return [subs[i * cells:(i + 1) * cells] for i in range(n_subs)]
+
+
+def compute_glcm_privatized(img: QuantizedImage, p: GlcmParams, plan_: ExecutionPlan,
+                            group_count: int = 0) -> Tuple[Glcm, ContentionStats]:
+    """parallel.hpp:240-254 — Scheme 2: counts from the privatised vote kernel,
+    per_copy_hottest from the reference-routed sub-GLCMs."""
+    _, counts, hottest, _ = _subglcms(img, p, plan_, group_count, False)
+    g = Glcm(p.levels, counts)
+    st = stats_from_counts(g)
+    st.per_copy_hottest = [int(x) for x in hottest]
+    return g, st
 
 
 def contention_profile(img: QuantizedImage, p: GlcmParams) -> ContentionStats:

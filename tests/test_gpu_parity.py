@@ -335,3 +335,42 @@ def test_two_pass_split_boundaries(engine, w):
         got = engine.glcm(gray, w, h, levels, dts)
         for t, (d, a) in enumerate(dts):
             assert np.array_equal(got[0, t].reshape(-1), O.glcm_gray(gray, w, h, levels, d, a)), (w, levels, d, a)
+
+
+def _subglcms_numpy(q, w, h, L, d, a, group_size, copies, groups):
+    """parallel.hpp:160-212 restated in numpy: stripe_rows(h, groups), stripe
+    pixel k -> lane (k - stripe_begin*w) % group_size -> copy lane % copies."""
+    dr, dc = {0: (0, d), 45: (d, -d), 90: (d, 0), 135: (d, d)}[a]
+    img = q.reshape(h, w).astype(np.int64)
+    base, extra = divmod(h, groups)
+    subs = np.zeros((groups, copies, L * L), np.uint32)
+    row = 0
+    c0, c1 = (d if dc < 0 else 0), (w - d if dc > 0 else w)
+    for g in range(groups):
+        end = row + base + (1 if g < extra else 0)
+        for r in range(row, min(end, h - dr)):
+            cols = np.arange(c0, c1)
+            anchor = img[r, cols]
+            ref = img[r + dr, cols + dc]
+            lane = ((r - row) * w + cols) % group_size
+            np.add.at(subs[g], (lane % copies, ref * L + anchor), 1)
+        row = end
+    return subs.reshape(groups * copies, L * L)
+
+
+@pytest.mark.parametrize("copies,groups", [(1, 1), (3, 4), (8, 7)])
+def test_python_subglcms_and_per_copy_hottest(copies, groups):
+    w, h, L = 97, 53, 16
+    q = O.quantize(tf.synth_noise(w, h, 21).pixels, L)
+    img = tf.QuantizedImage(w, h, L, q)
+    p = tf.GlcmParams(2, tf.Angle.deg135, L)
+    plan = tf.plan(L, tf.kDefaultScratchBudget, 3)
+    plan.copies = copies
+    got = tf.compute_subglcms(img, p, plan, groups)
+    want = _subglcms_numpy(q, w, h, L, 2, 135, plan.group_size, copies, groups)
+    assert len(got) == groups * copies
+    for i in range(len(got)):
+        assert np.array_equal(got[i], want[i]), i
+    g, st = tf.compute_glcm_privatized(img, p, plan, groups)
+    assert np.array_equal(g.counts, want.sum(axis=0).astype(np.uint64))
+    assert st.per_copy_hottest == [int(x) for x in want.max(axis=1)]
