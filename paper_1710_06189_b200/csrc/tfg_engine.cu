@@ -102,6 +102,9 @@ struct tfg_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t exec = nullptr, copy = nullptr;
+  static constexpr int kAux = 4;
+  cudaStream_t aux[kAux]{};              // fork streams of tfg_glcm_multi_async (L <= 64)
+  cudaEvent_t fork_ev = nullptr, join_ev[kAux]{};
   static constexpr int kSlots = 3;
   DevBuf dslot[kSlots];                  // device chunk ring
   HostBuf hslot[kSlots];                 // pinned chunk ring (chunk sources)
@@ -699,6 +702,11 @@ int tfg_ctx_create(tfg_ctx** out, int device, unsigned flags) {
     }
     ck(cudaMalloc(&ctx->d_err, 64), "cudaMalloc");
     ck(cudaMemset(ctx->d_err, 0, 64), "memset");
+    for (int i = 0; i < tfg_ctx::kAux; ++i) {
+      ck(cudaStreamCreateWithFlags(&ctx->aux[i], cudaStreamNonBlocking), "stream");
+      ck(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming), "event");
+    }
+    ck(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming), "event");
     ck(cudaMalloc(&ctx->sync_ctr, 64), "cudaMalloc");
   });
   if (rc != TFG_OK) {
@@ -735,6 +743,11 @@ void tfg_ctx_destroy(tfg_ctx* ctx) {
     }
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->sync_ctr) cudaFree(ctx->sync_ctr);
+    for (int i = 0; i < tfg_ctx::kAux; ++i) {
+      if (ctx->aux[i]) cudaStreamDestroy(ctx->aux[i]);
+      if (ctx->join_ev[i]) cudaEventDestroy(ctx->join_ev[i]);
+    }
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
     if (ctx->exec) cudaStreamDestroy(ctx->exec);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (prev >= 0) cudaSetDevice(prev);
@@ -1213,10 +1226,29 @@ int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
     if (pixel_levels == levels)
       launch_validate(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, levels, ctx->d_err, s);
     const size_t per_dt = n_bands * (size_t)levels * levels;
-    for (int t = 0; t < n_dt; ++t)
+    // L <= 64 launches share no scratch (direct u64 atomics, per-CTA smem
+    // tickets): fork them over the context's aux streams so one GLCM's
+    // prologue/epilogue and tail overlap another's votes (small images are
+    // launch- and tail-bound); L > 64 launches share the partials and the
+    // grid-barrier counter and stay ordered on `s`.
+    const bool fork = n_dt > 1 && (size_t)levels * levels <= 4096 && !(flags & TFG_SCHEME_GLOBAL);
+    if (fork) ck(cudaEventRecord(ctx->fork_ev, s), "event record");
+    for (int t = 0; t < n_dt; ++t) {
+      cudaStream_t st = s;
+      if (fork) {
+        st = ctx->aux[t % tfg_ctx::kAux];
+        if (t < tfg_ctx::kAux) ck(cudaStreamWaitEvent(st, ctx->fork_ev, 0), "wait");
+      }
       launch_vote(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, row_end, pixel_levels, levels,
                   distances[t], angles_deg[t], flags,
-                  reinterpret_cast<unsigned long long*>(d_counts) + (size_t)t * per_dt, s);
+                  reinterpret_cast<unsigned long long*>(d_counts) + (size_t)t * per_dt, st);
+    }
+    if (fork) {
+      for (int i = 0; i < std::min(n_dt, tfg_ctx::kAux); ++i) {
+        ck(cudaEventRecord(ctx->join_ev[i], ctx->aux[i]), "event record");
+        ck(cudaStreamWaitEvent(s, ctx->join_ev[i], 0), "wait");
+      }
+    }
   });
 }
 
