@@ -1,3 +1,6 @@
+# Full round evidence pass (run under gpurun): smoke, pytest -m gpu, C++ drop-in + reference suites,
+# CLI suite, bench (all BASELINE configs + reference arm), one-step ncu launch list, ncu --set full
+# summaries of the vote kernel, per-L kernel rates. Outputs in gpurun_out/r14/ (see profiles/README.md).
 mkdir -p gpurun_out/r14
 O=gpurun_out/r14
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,power.limit --format=csv > $O/info.txt 2>&1
