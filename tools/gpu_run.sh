@@ -23,8 +23,8 @@ for s in $stages; do
       for S in 1 2 3 4; do timeout 300 python tools/profile_vote.py --levels 32 --strategy $S --dts 1:0 --reps 5 --time > $OUT/timing_L32_s$S.json 2>&1; done
       for S in 3 4; do timeout 300 python tools/profile_vote.py --levels 128 --strategy $S --dts 1:0 --reps 5 --time > $OUT/timing_L128_s$S.json 2>&1; done ;;
     ncu)
-      # exactly one timed step of the default bench: skip the 4 earlier steps (1 check + 3 warm-up) x 48 engine launches
-      timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:tfg:: -s 192 -c 48 --csv --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_bench.json 2>&1
+      # exactly one timed step of the default bench: skip the 4 earlier steps (1 check + 3 warm-up) x 24 vote launches
+      timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:glcm -s 96 -c 24 --csv --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_bench.json 2>&1
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:glcm_ -c 4 -o $OUT/prof_c3 python tools/profile_vote.py --reps 1 --kinds noise,smooth > $OUT/ncu_full.log 2>&1 ;;
     ncu32)
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:glcm_vote_kernel -c 1 -o $OUT/prof_L32 python tools/profile_vote.py --levels 32 --kinds noise --reps 1 > $OUT/ncu_L32.log 2>&1
