@@ -385,6 +385,7 @@ def run_engine(args, wl):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        dist.barrier()  # every rank's communicator is up before the first P2P batch (halo exchange)
 
     plan = Plan(wl, world, rank, tf, D)
     eng = tf.Engine(local)

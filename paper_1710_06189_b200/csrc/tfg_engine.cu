@@ -165,8 +165,6 @@ void check_geometry(size_t width, size_t height, int distance) {
     fail(TFG_INVALID_ARGUMENT, "glcm: degenerate geometry (d must be in [1, min(width, height)))");
 }
 
-// 227 KB opt-in per CTA minus the kernel's static shared memory and slack.
-constexpr size_t kMaxHistBytes = 227 * 1024 - 256;
 
 int pick_strategy(int levels, unsigned flags) {
   const int forced = (int)((flags >> TFG_STRATEGY_SHIFT) & 0xF);

@@ -576,6 +576,25 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     const uint32_t row0 = fast_div(f0, p.ni_mul, p.ni_shr);
     const uint32_t jj0 = f0 - row0 * ni;
     const unsigned long long roff = (unsigned long long)row0 * pitch + (jj0 << 4);
+    if (jj0 + 64u <= ni) {
+      // warp-uniform common case (~94% at 16384 px rows): no row wrap inside
+      // the double batch, so both items of a lane share one pointer and the
+      // second sits at a +512 B immediate offset
+      const uint8_t* a = abase0 + roff + lane16;
+      x0.a = ldg16(a);
+      x1.a = ldg16(a + 512);
+      // KSEL >= 5 (theta = 0, d < 16): ref_off == 0, the reference row is the anchor row
+      const uint8_t* r = ksel_c0_is_anchor<KSEL>() ? a : rbase0 + roff + lane16;
+      if constexpr (!ksel_c0_is_anchor<KSEL>()) {
+        x0.c0 = ldg16(r);
+        x1.c0 = ldg16(r + 512);
+      }
+      if constexpr (ksel_needs_c1<KSEL>()) {
+        x0.c1 = ldg16(r + 16);
+        x1.c1 = ldg16(r + 528);
+      }
+      return;
+    }
     const uint32_t off0 = lane16 + (jj0 + lane >= ni ? wrap_off : 0u);  // ni >= 64: at most one wrap
     const uint32_t off1 = lane16 + 512u + (jj0 + lane + 32u >= ni ? wrap_off : 0u);
     const uint8_t* a = abase0 + roff;
@@ -606,7 +625,13 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     a1 = min(a1, (long long)p.buf_bytes);
     if (a1 > a0) prefetch_l2(band + a0, (uint32_t)min(a1 - a0, 1ll << 20) & ~15u);
   };
-  constexpr uint32_t kAhead = 48, kSpan = 16;
+#ifndef TFG_PREFETCH_AHEAD
+#define TFG_PREFETCH_AHEAD 48
+#endif
+#ifndef TFG_PREFETCH_SPAN
+#define TFG_PREFETCH_SPAN 16
+#endif
+  constexpr uint32_t kAhead = TFG_PREFETCH_AHEAD, kSpan = TFG_PREFETCH_SPAN;  // in double batches
   auto grab4 = [&]() -> uint32_t {
     uint32_t tn = 0;
     if (lane == 0) {
