@@ -59,6 +59,11 @@ WORKLOADS = {
                bands=1),
     "c1": dict(width=512, height=512, levels=(8,), ds=(1,), kinds=("noise",), layout="replica", bands=1,
                angles=(0,)),
+    # small test-only variants of the partitioned layouts (tests/test_bench_dist.py)
+    "t3": dict(width=4096, block_rows=1024, levels=(256,), ds=(1, 4), kinds=("noise", "smooth"),
+               layout="rows-weak", bands=1),
+    "t5": dict(width=4096, height=4096, levels=(64,), ds=(1,), kinds=("noise",), layout="rows-strong", bands=1),
+    "t4": dict(width=1024, height=1024, levels=(32,), ds=(1,), kinds=("noise",), layout="bands", bands=10),
 }
 GEN_BLOCK = 1024  # rows per generator block of the strong-scaling images (content independent of N)
 

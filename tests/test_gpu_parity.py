@@ -374,3 +374,31 @@ def test_python_subglcms_and_per_copy_hottest(copies, groups):
     g, st = tf.compute_glcm_privatized(img, p, plan, groups)
     assert np.array_equal(g.counts, want.sum(axis=0).astype(np.uint64))
     assert st.per_copy_hottest == [int(x) for x in want.max(axis=1)]
+
+
+@pytest.mark.parametrize("levels", [16, 64, 256])
+def test_multi_async_all_dts_bands_row_end(engine, levels):
+    # tfg_glcm_multi_async: every (d, theta) in one call; L <= 64 forks the
+    # launches over the context's aux streams, L > 64 stays ordered
+    import torch
+    w, h, nb, row_end = 1200, 300, 3, 280
+    imgs = [tf.synth_smooth(w, h, 40 + b).pixels if b % 2 else tf.synth_noise(w, h, 40 + b).pixels
+            for b in range(nb)]
+    pitch = 1216  # 16-byte aligned pitch > width
+    buf = np.zeros((nb, h, pitch), np.uint8)
+    for b in range(nb):
+        buf[b, :, :w] = imgs[b].reshape(h, w)
+    dev = torch.from_numpy(buf).cuda()
+    dts = [(1, 0), (2, 45), (3, 90), (4, 135), (7, 0)]
+    cells = levels * levels
+    out = torch.zeros(len(dts) * nb * cells, dtype=torch.int64, device="cuda")
+    d = (C.c_int * len(dts))(*[x[0] for x in dts])
+    a = (C.c_int * len(dts))(*[x[1] for x in dts])
+    s = torch.cuda.current_stream()
+    L.check(engine._lib.tfg_glcm_multi_async(engine.handle, C.c_void_p(dev.data_ptr()), w, h, pitch, pitch * h, nb,
+                                             row_end, 256, levels, d, a, len(dts), 0, C.c_void_p(out.data_ptr()),
+                                             C.c_void_p(s.cuda_stream)))
+    got = out.cpu().numpy().view(np.uint64).reshape(len(dts), nb, cells)
+    for t, (dd, aa) in enumerate(dts):
+        for b in range(nb):
+            assert np.array_equal(got[t, b], _oracle_rows(imgs[b], w, h, levels, dd, aa, row_end)), (t, b)
