@@ -386,7 +386,12 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   if (quant == tfg::Q_SHIFT && !(flags & TFG_SCHEME_GLOBAL)) {
     // the scaled side of a layout: ((v >> s) & m) << sc == (v >> (s - sc)) & (m << sc); s >= sc
     // holds because each layout is only used for L <= 2^(8 - sc).
-    p.qshift_scaled = p.qshift - tfg::strat_scale(pick_strategy(levels, flags));
+    const int strat = pick_strategy(levels, flags);
+    p.qshift_scaled = p.qshift - tfg::strat_scale(strat);
+    // reference side of item_words: COPIES8 scales it, the others do not
+    const bool ref_scaled = strat == tfg::S_COPIES8;
+    p.rshift = p.sbits + (ref_scaled ? p.qshift_scaled : p.qshift);
+    p.rmask = ref_scaled ? (p.qmask << tfg::strat_scale(strat)) : p.qmask;
   }
   const size_t cells = (size_t)levels * levels;
 

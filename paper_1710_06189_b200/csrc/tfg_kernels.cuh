@@ -73,6 +73,8 @@ struct VoteParams {
   uint32_t qmask;                   // Q_SHIFT / Q_CLAMP per-byte mask (L-1)*0x01010101
   int qshift;                       // Q_SHIFT: s = 8 - log2 L
   int qshift_scaled;                // Q_SHIFT: s - strat_scale
+  int rshift;                       // Q_SHIFT: sbits + the reference side's quantisation shift (item_words)
+  uint32_t rmask;                   // Q_SHIFT: the reference side's byte mask
   int hist_words;                   // shared-memory words
   unsigned long long* glcm;         // band b accumulator at glcm + b*L*L
   uint32_t* partials;               // null -> direct u64 atomics; else [band][grid][L*L]
@@ -380,6 +382,38 @@ __device__ __forceinline__ void ref_words(const VoteParams& p, const RawItem& it
   }
 }
 
+// P/Q words of an item with the reference side's power-of-two quantisation
+// folded into its funnel shift: (funnel(lo, hi, sbits) >> t) & M ==
+// funnel(lo, hi, sbits + t) & M, because the bits the wider shift pulls in
+// from the next byte land above the mask (sbits + t <= 31). Saves one shift
+// per word; other quantisers and the aligned case (KSEL 4) use the plain path.
+template <int QUANT, int STRAT, int KSEL>
+__device__ __forceinline__ void item_words(const VoteParams& p, const RawItem& it, uint32_t (&P)[4],
+                                           uint32_t (&Q)[4]) {
+  if constexpr (QUANT == Q_SHIFT && KSEL != 4) {
+    constexpr int sc = strat_scale(STRAT);
+    const uint4 c0 = ksel_c0_is_anchor<KSEL>() ? it.a : it.c0;
+    constexpr int k = KSEL >= 5 ? KSEL - 5 : KSEL;
+    const uint32_t W[8] = {c0.x, c0.y, c0.z, c0.w, it.c1.x, it.c1.y, it.c1.z, it.c1.w};
+    const uint32_t A[4] = {it.a.x, it.a.y, it.a.z, it.a.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t rq = __funnelshift_r(W[i + k], W[i + k + 1], p.rshift) & p.rmask;
+      if constexpr (STRAT == S_COPIES8) {  // reference side scaled, anchor-major cells
+        P[i] = rq;
+        Q[i] = quant4<QUANT>(A[i], p);
+      } else {
+        P[i] = quant4_scaled<QUANT, sc>(A[i], p);
+        Q[i] = rq;
+      }
+    }
+  } else {
+    uint32_t A[4], R[4];
+    ref_words<KSEL>(p, it, A, R);
+    prep_words<QUANT, STRAT>(p, A, R, P, Q);
+  }
+}
+
 // Generic cell words for Scheme 1: u16 lanes cell = ref*L + anchor.
 template <int QUANT>
 __device__ __forceinline__ void cells_of(const VoteParams& p, const uint32_t (&A)[4],
@@ -518,9 +552,8 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   uint32_t nb = 0;
   // Votes one item (16 pairs, or the pairs in `mask`).
   auto vote_item = [&](const RawItem& cur) {
-    uint32_t A[4], R[4], P[4], Q[4];
-    ref_words<KSEL>(p, cur, A, R);
-    prep_words<QUANT, STRAT>(p, A, R, P, Q);
+    uint32_t P[4], Q[4];
+    item_words<QUANT, STRAT, KSEL>(p, cur, P, Q);
     if constexpr (STRAT == S_PACKED16) {
       const bool check = rle || (nb & 7) == 0;
       const bool hit = vote16<STRAT>(hb, P, Q, cur.mask, check, glcm, L);
@@ -539,9 +572,8 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
 
   // An unmasked item of the main pass (all 16 pairs vote).
   auto vote_full = [&](const RawItem& cur) {
-    uint32_t A[4], R[4], P[4], Q[4];
-    ref_words<KSEL>(p, cur, A, R);
-    prep_words<QUANT, STRAT>(p, A, R, P, Q);
+    uint32_t P[4], Q[4];
+    item_words<QUANT, STRAT, KSEL>(p, cur, P, Q);
     if constexpr (STRAT == S_PACKED16) {
       const bool check = rle || (nb & 7) == 0;
       const bool hit = vote16<STRAT>(hb, P, Q, 0xFFFFu, check, glcm, L);
