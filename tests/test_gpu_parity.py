@@ -402,3 +402,22 @@ def test_multi_async_all_dts_bands_row_end(engine, levels):
     for t, (dd, aa) in enumerate(dts):
         for b in range(nb):
             assert np.array_equal(got[t, b], _oracle_rows(imgs[b], w, h, levels, dd, aa, row_end)), (t, b)
+
+
+@pytest.mark.parametrize("pattern", ["constant", "alternating", "stripes"])
+def test_packed16_drains_exact(engine, pattern):
+    # > 2^15 votes per CTA on single cells (8192^2 / 148 CTAs ~ 450K votes
+    # each): the PACKED16 drain path runs many times, through the run-length
+    # votes (constant), through plain votes with both u16 halves (alternating:
+    # no 16-pixel item is uniform), and with a hot cell per half (stripes)
+    w = h = 8192
+    if pattern == "constant":
+        img = np.full(w * h, 200, np.uint8)
+    elif pattern == "alternating":
+        img = np.tile(np.array([10, 250], np.uint8), w * h // 2)
+    else:
+        row = np.where((np.arange(w) // 3) % 2 == 0, 7, 131).astype(np.uint8)
+        img = np.tile(row, h)
+    for d, a in [(1, 0), (1, 90), (2, 45), (3, 135)]:
+        got = engine.glcm(img, w, h, 256, [(d, a)])
+        assert np.array_equal(got.reshape(-1), O.glcm_serial(img, w, h, 256, d, a)), (pattern, d, a)
