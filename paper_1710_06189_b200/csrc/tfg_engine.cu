@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -245,6 +246,24 @@ VoteKernel pick_global(int quant, int ksel) {
   }
 }
 
+// Shared tail pool of the cooperative vote launches: per-band counters sit
+// 128 bytes past the grid-barrier counter (its own L2 line), in one memset.
+constexpr size_t kPoolCtrOffset = 32;
+constexpr int kMaxPoolBands = 1024;
+#ifndef TFG_POOL_PCT
+#define TFG_POOL_PCT 20
+#endif
+// Percentage of the interior items in the pool (TEXFORGE_POOL_PCT overrides
+// it for tuning; 0 disables the pool).
+long long pool_pct() {
+  static const long long v = [] {
+    const char* e = std::getenv("TEXFORGE_POOL_PCT");
+    const long long x = e ? std::atoll(e) : (long long)TFG_POOL_PCT;
+    return std::min<long long>(std::max<long long>(x, 0), 90);
+  }();
+  return v;
+}
+
 // Every vote kernel gets the full 227 KB dynamic shared-memory opt-in once;
 // occupancy is then queried per (kernel, smem) pair.
 std::mutex g_kinfo_mu;
@@ -345,6 +364,9 @@ VoteGeometry make_geometry(size_t width, size_t height, size_t pitch, size_t row
   }
   p.main_items = (long long)nrows * p.ni;
   p.edge_items = (long long)nrows * p.ne;
+  p.pool_beg = p.main_items;  // no shared pool unless launch_vote sets one
+  p.pool_dbl = 0;
+  p.pool_ctr = nullptr;
   fastdiv_consts((uint32_t)std::max(p.ni, 1), &p.ni_mul, &p.ni_shr);
   fastdiv_consts((uint32_t)p.ne, &p.ne_mul, &p.ne_shr);
   // quantisation mode
@@ -421,9 +443,23 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
                                        : std::max<long long>(1, (8 * slots + n_bands - 1) / n_bands);
   per_band = std::min<long long>(per_band, (p.items + 2 * tfg::kThreads - 1) / (2 * tfg::kThreads));
   per_band = std::max<long long>(per_band, 1);
-  p.main_per_cta = ((p.main_items + per_band - 1) / per_band + 63) / 64 * 64;
-  p.edge_per_cta = (p.edge_items + per_band - 1) / per_band;
   const bool use_partials = cells > 4096;
+  // With partials and a grid that is co-resident (one CTA per SM slot), the
+  // kernel reduces the partials itself behind a grid barrier (cooperative
+  // launch guarantees co-residency); larger grids use the reduce kernels.
+  const bool in_kernel_reduce = use_partials && per_band * n_bands <= (long long)ctx->num_sms * bps;
+  if (in_kernel_reduce && n_bands <= kMaxPoolBands &&
+      (strat == tfg::S_PACKED16 || strat == tfg::S_COPY1)) {  // the layouts with the pool loop
+    // The grid barrier waits for the slowest CTA, so the last pool_pct % of
+    // each band's interior items go to a shared pool that CTAs drain after
+    // their own contiguous range (counters zeroed with the barrier's).
+    const long long pool = p.main_items * pool_pct() / 100 / 256 * 4;  // whole grabs
+    p.pool_dbl = (uint32_t)std::min<long long>(pool, 1 << 24);
+    p.pool_beg = p.main_items - 64LL * p.pool_dbl;
+    p.pool_ctr = ctx->sync_ctr + kPoolCtrOffset;
+  }
+  p.main_per_cta = ((p.pool_beg + per_band - 1) / per_band + 63) / 64 * 64;
+  p.edge_per_cta = (p.edge_items + per_band - 1) / per_band;
   const bool packed_partials = use_partials && strat == tfg::S_PACKED16;
   if (use_partials) {
     const size_t per_cta = packed_partials ? words : cells;
@@ -431,13 +467,11 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
     p.partials = static_cast<uint32_t*>(ctx->partials.get(bytes));
   }
   dim3 grid((unsigned)per_band, (unsigned)n_bands);
-  // With partials and a grid that is co-resident (one CTA per SM slot), the
-  // kernel reduces the partials itself behind a grid barrier (cooperative
-  // launch guarantees co-residency); larger grids use the reduce kernels.
-  const bool in_kernel_reduce = use_partials && per_band * n_bands <= (long long)ctx->num_sms * bps;
   if (in_kernel_reduce) {
     p.sync_ctr = ctx->sync_ctr;
-    ck(cudaMemsetAsync(ctx->sync_ctr, 0, sizeof(unsigned int), s), "memset");
+    const size_t ctr_bytes = p.pool_ctr ? (kPoolCtrOffset + (size_t)n_bands) * sizeof(unsigned int)
+                                        : sizeof(unsigned int);
+    ck(cudaMemsetAsync(ctx->sync_ctr, 0, ctr_bytes, s), "memset");
     void* args[] = {&p};
     ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), grid, dim3(tfg::kThreads), args, smem, s),
        "glcm_vote_kernel cooperative launch");
@@ -710,7 +744,7 @@ int tfg_ctx_create(tfg_ctx** out, int device, unsigned flags) {
       ck(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming), "event");
     }
     ck(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming), "event");
-    ck(cudaMalloc(&ctx->sync_ctr, 64), "cudaMalloc");
+    ck(cudaMalloc(&ctx->sync_ctr, (kPoolCtrOffset + kMaxPoolBands) * sizeof(unsigned int)), "cudaMalloc");
   });
   if (rc != TFG_OK) {
     tfg_ctx_destroy(ctx);

@@ -14,8 +14,9 @@
 // 16-pixel "items" (one 16-byte vector per row segment). A main pass votes the
 // interior segments of every row in double batches of 64 consecutive items
 // (lanes l and l+32; every LDG.128 of the warp is one coalesced 512-byte
-// access) taken from a per-CTA ticket counter, two double batches in a
-// register ring; an edge pass votes the row ends with masks. The reference
+// access), four per grab from a per-CTA ticket counter and then, when the
+// launch is cooperative, from the band's shared tail pool; two double batches
+// sit in a register ring. An edge pass votes the row ends with masks. The reference
 // neighbour of each segment is one or two aligned 16-byte loads + funnel
 // shifts (displacement dcol = 16q + 4k + s: q and the word shift k are launch
 // / template constants, s is a byte funnel shift).
@@ -84,8 +85,13 @@ struct VoteParams {
   int ni;                           // interior segments per row (0: everything is edge work)
   uint32_t ni_mul, ni_shr;          // fast division by ni
   long long main_items;             // nrows * ni
-  long long main_per_cta;           // multiple of 64
-  int ne;                           // edge segments per row (2, or nch when ni == 0)
+  long long main_per_cta;           // multiple of 64; CTA ranges tile [0, pool_beg)
+  // shared tail pool (cooperative launches): interior items [pool_beg, main_items)
+  // = pool_dbl double batches handed to any CTA of the band from pool_ctr[band]
+  long long pool_beg;               // == main_items: no pool
+  uint32_t pool_dbl;
+  unsigned int* pool_ctr;           // zeroed before the launch; null: no pool
+  int ne;                       // edge segments per row (2, or nch when ni == 0)
   uint32_t ne_mul, ne_shr;          // fast division by ne
   long long edge_items;             // nrows * ne
   long long edge_per_cta;
@@ -514,9 +520,11 @@ __device__ __forceinline__ void reduce_partials_slice(const VoteParams& p, uint3
 //    row, so these loads need no guards and all 16 pairs vote:
 //    no masks, no per-pair branches. A warp takes "double batches" of 64
 //    consecutive segments (lane and lane+32; each LDG.128 of the warp is one
-//    coalesced 512-byte access) from a per-CTA ticket counter, two per grab,
+//    coalesced 512-byte access) from a per-CTA ticket counter, four per grab,
 //    and keeps two double batches in a register ring (one in flight while the
-//    other votes). Addresses come from one uniform division per double batch
+//    other votes). In cooperative launches the last pool_dbl double batches
+//    of the band form a shared pool that CTAs drain once their own range is
+//    done, so the grid barrier does not wait on the slowest static range. Addresses come from one uniform division per double batch
 //    plus a per-lane row-wrap select.
 //  * edge pass — the first and last segment of every row (or every segment
 //    of a narrow image), with per-lane guarded loads and valid-anchor masks.
@@ -589,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
 
   // ---------------- main pass: interior segments, 64 per double batch -------
   const long long mbeg64 = (long long)blockIdx.x * p.main_per_cta;
-  const long long mend64 = min(mbeg64 + p.main_per_cta, p.main_items);
+  const long long mend64 = min(mbeg64 + p.main_per_cta, p.pool_beg);
   const uint32_t mbeg = (uint32_t)mbeg64;
   const uint32_t m_items = mend64 > mbeg64 ? (uint32_t)(mend64 - mbeg64) : 0u;
   const uint32_t wrap_off = pitch - ni * 16u;  // next row, back to interior segment 0
@@ -603,8 +611,8 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   // one 32-bit lane offset
   const uint8_t* const abase0 = band + ((p.ch0 + 1) << 4);
   const uint8_t* const rbase0 = abase0 + p.ref_off;
-  auto issue_dbl = [&](uint32_t t, RawItem& x0, RawItem& x1) {
-    const uint32_t f0 = mbeg + t * 64;                       // warp-uniform
+  // f0: first item of the double batch (warp-uniform)
+  auto issue_dbl = [&](uint32_t f0, RawItem& x0, RawItem& x1) {
     const uint32_t row0 = fast_div(f0, p.ni_mul, p.ni_shr);
     const uint32_t jj0 = f0 - row0 * ni;
     const unsigned long long roff = (unsigned long long)row0 * pitch + (jj0 << 4);
@@ -675,37 +683,77 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
 
   RawItem a0, a1, b0i, b1i;
   uint32_t ta = 2 * warp, tb = 2 * warp + 1;
-  if (ta < n_full_dbl) issue_dbl(ta, a0, a1);
-  if (tb < n_full_dbl) issue_dbl(tb, b0i, b1i);
+  if (ta < n_full_dbl) issue_dbl(mbeg + ta * 64, a0, a1);
+  if (tb < n_full_dbl) issue_dbl(mbeg + tb * 64, b0i, b1i);
   if (tid == 0) {
     s_ticket = 2 * kWarps;
     for (uint32_t q = 0; q < kAhead + kSpan; q += kSpan) prefetch_span(q + 2 * kWarps, kSpan);
   }
   __syncthreads();  // histogram zeroed, ticket counter set
 
-  auto vote_dbl = [&](uint32_t, const RawItem& x0, const RawItem& x1) {
-    vote_full(x0);
-    vote_full(x1);
-  };
   // one ticket grab (4 double batches) per two revolutions of the ring
   for (;;) {
     if (ta >= n_full_dbl) break;
-    vote_dbl(ta, a0, a1);
+    vote_full(a0);
+    vote_full(a1);
     const uint32_t tn = grab4();
     ta = tn;
-    if (ta < n_full_dbl) issue_dbl(ta, a0, a1);
+    if (ta < n_full_dbl) issue_dbl(mbeg + ta * 64, a0, a1);
     if (tb >= n_full_dbl) break;
-    vote_dbl(tb, b0i, b1i);
+    vote_full(b0i);
+    vote_full(b1i);
     tb = tn + 1;
-    if (tb < n_full_dbl) issue_dbl(tb, b0i, b1i);
+    if (tb < n_full_dbl) issue_dbl(mbeg + tb * 64, b0i, b1i);
     if (ta >= n_full_dbl) break;
-    vote_dbl(ta, a0, a1);
+    vote_full(a0);
+    vote_full(a1);
     ta = tn + 2;
-    if (ta < n_full_dbl) issue_dbl(ta, a0, a1);
+    if (ta < n_full_dbl) issue_dbl(mbeg + ta * 64, a0, a1);
     if (tb >= n_full_dbl) break;
-    vote_dbl(tb, b0i, b1i);
+    vote_full(b0i);
+    vote_full(b1i);
     tb = tn + 3;
-    if (tb < n_full_dbl) issue_dbl(tb, b0i, b1i);
+    if (tb < n_full_dbl) issue_dbl(mbeg + tb * 64, b0i, b1i);
+  }
+
+  // Shared tail pool (cooperative launches): once its own range is done, a
+  // warp takes four double batches [g, g + 256) per grab from the band's
+  // global counter (the pool is a whole number of grabs). The counter only
+  // grows, so the first empty grab ends the warp's main pass. Only the
+  // layouts with per-CTA partials (L > 64) end at a grid barrier, so only
+  // they carry this loop.
+  if constexpr (STRAT == S_PACKED16 || STRAT == S_COPY1) {
+    if (p.pool_ctr) {
+      constexpr uint32_t kNone = 0xFFFFFFFFu;
+      auto grab_pool = [&]() -> uint32_t {
+        uint32_t g = kNone;
+        if (lane == 0) {
+          const uint32_t tp = atomicAdd(p.pool_ctr + band_idx, 4u);
+          if (tp < p.pool_dbl) g = (uint32_t)p.pool_beg + tp * 64;
+        }
+        return __shfl_sync(0xffffffffu, g, 0);
+      };
+      uint32_t g = grab_pool();
+      if (g != kNone) {
+        issue_dbl(g, a0, a1);
+        issue_dbl(g + 64, b0i, b1i);
+      }
+      while (g != kNone) {
+        vote_full(a0);
+        vote_full(a1);
+        issue_dbl(g + 128, a0, a1);
+        vote_full(b0i);
+        vote_full(b1i);
+        issue_dbl(g + 192, b0i, b1i);
+        vote_full(a0);
+        vote_full(a1);
+        g = grab_pool();
+        if (g != kNone) issue_dbl(g, a0, a1);
+        vote_full(b0i);
+        vote_full(b1i);
+        if (g != kNone) issue_dbl(g + 64, b0i, b1i);
+      }
+    }
   }
 
   // ---------------- edge pass: first/last segment of each row (or all) -----

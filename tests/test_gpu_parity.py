@@ -421,3 +421,36 @@ def test_packed16_drains_exact(engine, pattern):
     for d, a in [(1, 0), (1, 90), (2, 45), (3, 135)]:
         got = engine.glcm(img, w, h, 256, [(d, a)])
         assert np.array_equal(got.reshape(-1), O.glcm_serial(img, w, h, 256, d, a)), (pattern, d, a)
+
+
+_POOL_SCRIPT = r"""
+import numpy as np
+from oracle import oracle as O
+from paper_1710_06189_b200 import texforge as tf
+eng = tf.Engine(0)
+dts = [(1, 0), (3, 45), (2, 90), (1, 135)]
+for w, h, nb, levels in [(4096, 777, 1, 256), (3001, 301, 3, 256), (2048, 513, 2, 128), (1100, 2000, 1, 100)]:
+    imgs = [tf.synth_noise(w, h, 7 * w + b).pixels for b in range(nb)]
+    got = eng.glcm(np.concatenate(imgs), w, h, levels, dts, n_bands=nb)
+    for b in range(nb):
+        for t, (d, a) in enumerate(dts):
+            ref = O.glcm_gray(imgs[b], w, h, levels, d, a)
+            assert np.array_equal(got[b, t].reshape(-1), ref), (w, h, nb, levels, b, d, a)
+print("POOL-OK")
+"""
+
+
+@pytest.mark.parametrize("pct", [0, 3, 90])
+def test_shared_tail_pool_fractions(pct):
+    # cooperative launches (L*L > 4096, co-resident grid) hand the last
+    # TEXFORGE_POOL_PCT % of each band's interior items to a shared pool; the
+    # counts must not depend on how much work goes through it (read once per
+    # process, hence the subprocess)
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TEXFORGE_POOL_PCT=str(pct), PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _POOL_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "POOL-OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
