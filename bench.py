@@ -164,16 +164,33 @@ def committed_traffic(workload):
 
 
 # --------------------------------------------------------------------------- inputs
+def noise_pixels(tf, width, height, seed):
+    """synth_noise(width, height, seed) pixels, generated on the device
+    (tfg_synth_noise_device: mt19937 jump-ahead, bit-identical to the host
+    generator) and copied back; inputs are untimed, this only shortens setup."""
+    import torch
+    if torch.cuda.is_available():
+        dev = torch.cuda.current_device()
+        eng = _GEN_ENGINES.get(dev) or _GEN_ENGINES.setdefault(dev, tf.Engine(dev))
+        return eng.synth_noise_device(width, height, seed).cpu().numpy()
+    return tf.synth_noise(width, height, seed).pixels
+
+
+_GEN_ENGINES = {}
+
+
 def gen_rows(tf, kind, width, row0, rows, block_rows, seed0):
     """Rows [row0, row0+rows) of an image made of generator blocks of
     `block_rows` rows, block b = synth_<kind>(width, block_rows, seed0 + b).
     The content does not depend on how the rows are later partitioned."""
-    gen = tf.synth_noise if kind == "noise" else tf.synth_smooth
     out = np.empty(rows * width, dtype=np.uint8)
     r = row0
     while r < row0 + rows:
         b = r // block_rows
-        blk = gen(width, block_rows, seed0 + b).pixels
+        if kind == "noise":
+            blk = noise_pixels(tf, width, block_rows, seed0 + b)
+        else:
+            blk = tf.synth_smooth(width, block_rows, seed0 + b).pixels
         lo = r - b * block_rows
         hi = min(block_rows, row0 + rows - b * block_rows)
         out[(r - row0) * width:(r - row0 + hi - lo) * width] = blk[lo * width:hi * width]
@@ -260,13 +277,14 @@ def make_host_inputs(plan, tf):
     imgs = {}
     for kind in plan.kinds:
         if plan.layout == "bands":
-            imgs[kind] = np.concatenate([tf.synth_noise(plan.width, plan.height, b + 1).pixels
+            imgs[kind] = np.concatenate([noise_pixels(tf, plan.width, plan.height, b + 1)
                                          for b in plan.band_ids])
         elif plan.layout.startswith("rows"):
             imgs[kind] = gen_rows(tf, kind, plan.width, plan.owned0, plan.owned, plan.gen_block, 1)
+        elif kind == "noise":
+            imgs[kind] = noise_pixels(tf, plan.width, plan.height, 1)
         else:
-            gen = tf.synth_noise if kind == "noise" else tf.synth_smooth
-            imgs[kind] = gen(plan.width, plan.height, 1).pixels
+            imgs[kind] = tf.synth_smooth(plan.width, plan.height, 1).pixels
     return imgs
 
 

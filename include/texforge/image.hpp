@@ -7,7 +7,9 @@
 //                    points never need it: they fuse q = (v*L)>>8 into the vote.
 //   synth_*       -> libtexforge_cuda.so host generators (bit-identical to the
 //                    reference's mt19937 / std::sin sequences; synth_smooth
-//                    generates rows on every host thread).
+//                    generates rows on every host thread, synth_noise splits
+//                    the mt19937 sequence by jump-ahead across them).
+//                    tfg_synth_noise_device generates synth_noise in HBM.
 
 #include <cstddef>
 #include <cstdint>

@@ -108,6 +108,26 @@ int tfg_plan(int levels, size_t scratch_budget, unsigned worker_count, unsigned*
 int tfg_synth_noise(size_t width, size_t height, uint32_t seed, uint8_t* out);
 int tfg_synth_smooth(size_t width, size_t height, uint32_t seed, uint8_t* out, int threads);
 
+/* std::mt19937 jump-ahead (replaces stepping the reference's sequential
+ * generator, image.hpp:109-116). Writes `count` generator windows of 624
+ * words, window s at output index first + s*stride of std::mt19937(seed):
+ * a generator whose state array is that window emits outputs k, k+1, ...
+ * after one twist. Host only; threads <= 0: all hardware threads. */
+int tfg_mt19937_windows(uint32_t seed, uint64_t first, uint64_t stride, size_t count, uint32_t* out,
+                        int threads);
+
+/* synth_noise over n pixels on `threads` host threads (<= 0: all), each
+ * segment generated from its jump-ahead window; bit-identical to the
+ * sequential generator. tfg_synth_noise uses it for images >= 4 Mpixel. */
+int tfg_synth_noise_parallel(size_t n, uint32_t seed, uint8_t* out, int threads);
+
+/* synth_noise (image.hpp:109-116) generated ON THE DEVICE, bit-identical:
+ * pixel (y, x) of the width x height image -> d_out[y*pitch + x]. Segments of
+ * the generator sequence run in parallel from jump-ahead windows. Returns
+ * after the kernel has finished on `stream`. */
+int tfg_synth_noise_device(tfg_ctx* ctx, size_t width, size_t height, uint32_t seed, uint8_t* d_out,
+                           size_t pitch, void* stream);
+
 /* ---- the hot path ---------------------------------------------------------- */
 
 /* quantize (image.hpp:55-62) on the device; gray/out host or device per flags */

@@ -8,6 +8,7 @@
 //   tfg_glcm_bands    <- a loop of single-image calls in the reference
 //   tfg_symmetrize / tfg_normalize / tfg_features <- glcm.hpp:150-177, features.hpp:37-69
 //   tfg_quantize      <- quantize (image.hpp:55-62)
+//   tfg_synth_noise_device <- synth_noise (image.hpp:109-116), on the device
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -111,6 +112,7 @@ struct tfg_ctx {
   HostBuf hslot[kSlots];                 // pinned chunk ring (chunk sources)
   cudaEvent_t copied[kSlots]{}, consumed[kSlots]{};
   DevBuf img;                            // aligned copy of a device/host image
+  DevBuf mtwin;                          // synth_noise_device: generator windows per segment
   DevBuf acc;                            // u64 accumulators
   DevBuf sym, probs, feats;              // post-processing outputs
   DevBuf partials;                       // per-CTA sub-GLCMs (large L)
@@ -1315,6 +1317,34 @@ int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned 
         ctx->launches++;
       }
     }
+  });
+}
+
+int tfg_synth_noise_device(tfg_ctx* ctx, size_t width, size_t height, uint32_t seed, uint8_t* d_out,
+                           size_t pitch, void* stream) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded([&] {
+    if (width < 2 || height < 2) fail(TFG_INVALID_ARGUMENT, "synth_noise: dimensions must be >= 2");
+    if (!d_out || pitch < width) fail(TFG_INVALID_ARGUMENT, "synth_noise_device: null output or pitch < width");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned long long n = (unsigned long long)width * height;
+    // up to ~4 segments per SM (each a serial chain of 624-output twists) of
+    // >= ~1M outputs: each window costs ~4 ms of host jump-ahead per thread
+    const unsigned long long per = (n + (unsigned long long)ctx->num_sms * 4 - 1) / ((unsigned long long)ctx->num_sms * 4);
+    const unsigned long long seglen = std::max<unsigned long long>(624ull * 1680, (per + 623) / 624 * 624);
+    const size_t nseg = (size_t)((n + seglen - 1) / seglen);
+    std::vector<uint32_t> win(nseg * 624);
+    const int rc = tfg_mt19937_windows(seed, 0, seglen, nseg, win.data(), 0);
+    if (rc != TFG_OK) fail(rc, "synth_noise_device: generator jump-ahead failed");
+    uint32_t* d_win = static_cast<uint32_t*>(ctx->mtwin.get(win.size() * sizeof(uint32_t)));
+    ck(cudaMemcpyAsync(d_win, win.data(), win.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s), "H2D");
+    tfg::synth_noise_kernel<<<(unsigned)nseg, 256, 0, s>>>(d_win, seglen, n, width, pitch, d_out);
+    ck(cudaGetLastError(), "synth_noise_kernel launch");
+    ctx->launches++;
+    // the window buffer is reused by the next call: finish before returning
+    ck(cudaStreamSynchronize(s), "sync");
   });
 }
 

@@ -1151,4 +1151,56 @@ __global__ void __launch_bounds__(1024) features_kernel(const double* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device synth_noise (image.hpp:109-116: pixel k = mt19937(seed)() >> 24, k in
+// row-major order). CTA s regenerates outputs [s*seglen, (s+1)*seglen) from
+// the generator window the host computed by jump-ahead (tfg_mt19937.cpp):
+// each 624-output block is one in-place twist in three dependency phases
+// ([0,227) reads only old words, [227,454) and [454,624) read words of the
+// previous phase), then tempering. Bit-identical to the sequential generator.
+__device__ __forceinline__ uint32_t mt_twist(uint32_t x0, uint32_t x1, uint32_t xm) {
+  const uint32_t y = (x0 & 0x80000000u) | (x1 & 0x7FFFFFFFu);
+  return xm ^ (y >> 1) ^ ((y & 1u) ? 0x9908B0DFu : 0u);
+}
+
+__device__ __forceinline__ uint32_t mt_temper(uint32_t y) {
+  y ^= y >> 11;
+  y ^= (y << 7) & 0x9D2C5680u;
+  y ^= (y << 15) & 0xEFC60000u;
+  return y ^ (y >> 18);
+}
+
+__global__ void __launch_bounds__(256) synth_noise_kernel(const uint32_t* __restrict__ windows,
+                                                          unsigned long long seglen, unsigned long long n,
+                                                          unsigned long long width, unsigned long long pitch,
+                                                          uint8_t* __restrict__ out) {
+  __shared__ uint32_t mt[624];
+  const int t = threadIdx.x;
+  const unsigned long long k0 = (unsigned long long)blockIdx.x * seglen;
+  const unsigned long long k1 = min(k0 + seglen, n);
+  for (int i = t; i < 624; i += 256) mt[i] = windows[(size_t)blockIdx.x * 624 + i];
+  __syncthreads();
+  for (unsigned long long k = k0; k < k1; k += 624) {
+    uint32_t v = 0;
+    if (t < 227) v = mt_twist(mt[t], mt[t + 1], mt[t + 397]);
+    __syncthreads();
+    if (t < 227) mt[t] = v;
+    __syncthreads();
+    if (t < 227) v = mt_twist(mt[227 + t], mt[228 + t], mt[t]);
+    __syncthreads();
+    if (t < 227) mt[227 + t] = v;
+    __syncthreads();
+    if (t < 170) v = mt_twist(mt[454 + t], mt[t == 169 ? 0 : 455 + t], mt[227 + t]);
+    __syncthreads();
+    if (t < 170) mt[454 + t] = v;
+    __syncthreads();
+    const int cnt = (int)min(624ull, k1 - k);
+    for (int i = t; i < cnt; i += 256) {
+      const unsigned long long q = k + i, row = q / width;
+      out[row * pitch + (q - row * width)] = (uint8_t)(mt_temper(mt[i]) >> 24);
+    }
+    __syncthreads();  // the next twist overwrites mt
+  }
+}
+
 }  // namespace tfg

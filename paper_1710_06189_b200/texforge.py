@@ -275,6 +275,21 @@ class Engine:
     def launches(self) -> int:
         return int(self._lib.tfg_launch_count(self.handle))
 
+    def synth_noise_device(self, width: int, height: int, seed: int, out=None, pitch: int = 0, stream=None):
+        """image.hpp:109-116 generated on the device (bit-identical to
+        synth_noise). Returns a CUDA uint8 tensor of height*pitch bytes
+        (pitch = width unless given), or fills `out` (a CUDA tensor)."""
+        import torch
+        pitch = int(pitch or width)
+        if out is None:
+            out = torch.empty(height * pitch, dtype=torch.uint8, device=f"cuda:{self.device}")
+        if not out.is_cuda or out.numel() < height * pitch:
+            raise ValueError("synth_noise_device: out must be a CUDA tensor of >= height*pitch bytes")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        L.check(self._lib.tfg_synth_noise_device(self.handle, int(width), int(height), seed & 0xFFFFFFFF,
+                                                 C.c_void_p(out.data_ptr()), pitch, C.c_void_p(s)))
+        return out
+
     # -- raw, multi-(d, theta) entry point -------------------------------------
     def glcm(self, pixels: np.ndarray, width: int, height: int, levels: int, dts: Sequence[Tuple[int, int]],
              pixel_levels: int = 256, flags: int = 0, n_bands: int = 1,
@@ -459,6 +474,15 @@ def synth_noise(width: int, height: int, seed: int) -> GrayImage:
     out = np.empty(width * height, dtype=np.uint8)
     L.check(L.load().tfg_synth_noise(width, height, seed & 0xFFFFFFFF, _ptr(out)))
     return GrayImage(width, height, out)
+
+
+def mt19937_windows(seed: int, first: int, stride: int, count: int) -> np.ndarray:
+    """Generator windows of std::mt19937(seed) at outputs first + s*stride
+    (tfg_mt19937_windows; host jump-ahead), shape (count, 624) uint32."""
+    out = np.empty((count, 624), dtype=np.uint32)
+    L.check(L.load().tfg_mt19937_windows(seed & 0xFFFFFFFF, int(first), int(stride), int(count),
+                                         out.ctypes.data_as(C.POINTER(C.c_uint32)), 0))
+    return out
 
 
 def synth_smooth(width: int, height: int, seed: int, threads: int = 0) -> GrayImage:

@@ -221,7 +221,7 @@ def test_product_synth_bit_identical(golden_hashes):
     """The engine's host input generators reproduce the reference's synth_* bytes."""
     from paper_1710_06189_b200 import texforge as tf
     for r in golden_hashes["synth"]:
-        if r["w"] * r["h"] > 4096 * 4096:
-            continue
+        if r["kind"] == "smooth" and r["w"] * r["h"] > 4096 * 4096:
+            continue  # noise is generated on every host thread (mt19937 jump-ahead): 16384^2 in ~0.3 s
         img = (tf.synth_noise if r["kind"] == "noise" else tf.synth_smooth)(r["w"], r["h"], r["seed"]).pixels
         assert O.fnv1a64_image(img) == r["fnv_u64view"], r
