@@ -21,4 +21,5 @@ for L in 32 64; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:glcm_vote_kernel -c 1 -o /tmp/fullL$L python tools/profile_vote.py --levels $L --kinds noise --reps 1 > $O/ncu_full_L$L.log 2>&1
   python tools/ncu_summary.py /tmp/fullL$L.ncu-rep > $O/ncu_vote_L${L}_noise.txt 2>&1
 done
+bash tools/synth_gpu.sh 2>/dev/null; cp -r gpurun_out/synth $O/ 2>/dev/null
 for L in 256 128 64 32 16 8; do timeout 300 python tools/profile_vote.py --levels $L --dts 1:0,1:45,2:90,4:135 --reps 5 --time > $O/kernel_L$L.json 2>&1; done
