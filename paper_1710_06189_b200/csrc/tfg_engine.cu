@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -107,6 +108,7 @@ struct tfg_ctx {
   static constexpr int kAux = 4;
   cudaStream_t aux[kAux]{};              // fork streams of tfg_glcm_multi_async (L <= 64)
   cudaEvent_t fork_ev = nullptr, join_ev[kAux]{};
+  cudaEvent_t band_ev = nullptr;         // host pipeline: a band's last votes enqueued (early D2H)
   static constexpr int kSlots = 3;
   DevBuf dslot[kSlots];                  // device chunk ring
   HostBuf hslot[kSlots];                 // pinned chunk ring (chunk sources)
@@ -547,8 +549,10 @@ int host_memory_kind(const void* p) {
 }
 
 // Post-processing of n GLCMs resident at d_counts; results to host buffers.
+// counts_done: leading GLCMs whose counts the host pipeline already sent to
+// the (pinned) counts_out on ctx->aux[0] (plain counts only).
 void finish(tfg_ctx* ctx, unsigned long long* d_counts, int n, int levels, unsigned flags,
-            uint64_t* counts_out, double* probs_out, double* feats_out, cudaStream_t s) {
+            uint64_t* counts_out, double* probs_out, double* feats_out, cudaStream_t s, size_t counts_done = 0) {
   const size_t cells = (size_t)levels * levels;
   unsigned long long* d_final = d_counts;
   if (flags & TFG_SYMMETRIC) {
@@ -582,13 +586,16 @@ void finish(tfg_ctx* ctx, unsigned long long* d_counts, int n, int levels, unsig
   char* h = static_cast<char*>(ctx->hout.get(b_counts + b_probs + b_feats + b_err + 64));
   // a pinned caller buffer receives the counts by DMA directly (no staging copy)
   const bool counts_direct = counts_out && host_memory_kind(counts_out) == 1;
-  ck(cudaMemcpyAsync(counts_direct ? static_cast<void*>(counts_out) : static_cast<void*>(h), d_final, b_counts,
-                     cudaMemcpyDeviceToHost, s),
+  const size_t b_done = counts_direct ? counts_done * cells * 8 : 0;
+  ck(cudaMemcpyAsync(counts_direct ? static_cast<void*>(reinterpret_cast<char*>(counts_out) + b_done)
+                                   : static_cast<void*>(h),
+                     reinterpret_cast<const char*>(d_final) + b_done, b_counts - b_done, cudaMemcpyDeviceToHost, s),
      "D2H counts");
   if (b_probs) ck(cudaMemcpyAsync(h + b_counts, d_probs, b_probs, cudaMemcpyDeviceToHost, s), "D2H probs");
   if (b_feats) ck(cudaMemcpyAsync(h + b_counts + b_probs, d_feats, b_feats, cudaMemcpyDeviceToHost, s), "D2H feats");
   if (b_err) ck(cudaMemcpyAsync(h + b_counts + b_probs + b_feats, d_errs, b_err, cudaMemcpyDeviceToHost, s), "D2H err");
   ck(cudaStreamSynchronize(s), "stream sync");
+  if (b_done) ck(cudaStreamSynchronize(ctx->aux[0]), "stream sync");
   if (b_err) {
     const int* e = reinterpret_cast<const int*>(h + b_counts + b_probs + b_feats);
     for (int i = 0; i < n; ++i)
@@ -675,7 +682,7 @@ template <typename Fetch>
 void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, int levels,
                   const int* distances, const int* angles, int n_dt, size_t k, unsigned flags,
                   unsigned long long* d_acc, Fetch&& fetch_rows, size_t total_rows = 0, size_t n_bands = 1,
-                  size_t acc_band_stride = 0) {
+                  size_t acc_band_stride = 0, const std::function<void(size_t)>& band_done = nullptr) {
   // The ring runs continuously over (band, chunk): band b+1's first copy
   // overlaps band b's last votes. Band b's GLCMs go to d_acc + b*acc_band_stride.
   const std::vector<uint64_t> specs = chunk_specs(width, height, distances, angles, n_dt, k, total_rows);
@@ -703,6 +710,7 @@ void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, i
       launch_vote(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, levels, distances[t],
                   angles[t], flags, d_acc + bnd * acc_band_stride + (size_t)t * levels * levels, ctx->exec);
     ck(cudaEventRecord(ctx->consumed[sl], ctx->exec), "event record");
+    if (band_done && i == k - 1) band_done(bnd);
     if (sequential) ck(cudaStreamSynchronize(ctx->exec), "stream sync");
   }
 }
@@ -746,6 +754,7 @@ int tfg_ctx_create(tfg_ctx** out, int device, unsigned flags) {
       ck(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming), "event");
     }
     ck(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ctx->band_ev, cudaEventDisableTiming), "event");
     ck(cudaMalloc(&ctx->sync_ctr, (kPoolCtrOffset + kMaxPoolBands) * sizeof(unsigned int)), "cudaMalloc");
   });
   if (rc != TFG_OK) {
@@ -787,6 +796,7 @@ void tfg_ctx_destroy(tfg_ctx* ctx) {
       if (ctx->join_ev[i]) cudaEventDestroy(ctx->join_ev[i]);
     }
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->band_ev) cudaEventDestroy(ctx->band_ev);
     if (ctx->exec) cudaStreamDestroy(ctx->exec);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (prev >= 0) cudaSetDevice(prev);
@@ -932,6 +942,27 @@ int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size
         for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, sp[3 * i + 2] - sp[3 * i]);
         for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->hslot[sl].get(max_rows * width + 64);
       }
+      // PCIe is full duplex: a band's counts go down to a pinned counts_out
+      // while later bands are still coming up (plain counts, several bands)
+      const bool early = n_bands > 1 && counts_out && host_memory_kind(counts_out) == 1 &&
+                         !(flags & (TFG_SYMMETRIC | TFG_NORMALIZE | TFG_FEATURES));
+      const size_t band_words = (size_t)n_dt * cells;
+      auto band_done = [&](size_t b) {
+        if (b + 1 >= n_bands) return;  // the last band goes with finish()
+        ck(cudaEventRecord(ctx->band_ev, ctx->exec), "event record");
+        ck(cudaStreamWaitEvent(ctx->aux[0], ctx->band_ev, 0), "wait");
+        ck(cudaMemcpyAsync(counts_out + b * band_words, d_acc + b * band_words, band_words * 8,
+                           cudaMemcpyDeviceToHost, ctx->aux[0]),
+           "D2H band counts");
+      };
+      // every exit (errors included) waits for the early copies into counts_out
+      struct AuxDrain {
+        cudaStream_t st;
+        bool on;
+        ~AuxDrain() {
+          if (on) cudaStreamSynchronize(st);
+        }
+      } drain{ctx->aux[0], early};
       run_pipeline(
           ctx, width, owned_rows, pixel_levels, levels, distances, angles_deg, n_dt, k, flags, d_acc,
           [&](size_t b, size_t, size_t start, size_t, size_t buf_end, int sl) -> const uint8_t* {
@@ -941,9 +972,10 @@ int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size
             parallel_memcpy(dst, src, (buf_end - start) * width);
             return dst;
           },
-          height, n_bands, (size_t)n_dt * cells);
+          height, n_bands, band_words, early ? std::function<void(size_t)>(band_done) : nullptr);
       if (pixel_levels == levels) check_async_flag(ctx, s);
-      finish(ctx, d_acc, (int)n_out, levels, flags, counts_out, probs_out, feats_out, s);
+      finish(ctx, d_acc, (int)n_out, levels, flags, counts_out, probs_out, feats_out, s,
+             early ? (n_bands - 1) * (size_t)n_dt : 0);
       return;
     }
 

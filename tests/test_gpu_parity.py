@@ -454,3 +454,27 @@ def test_shared_tail_pool_fractions(pct):
     r = subprocess.run([sys.executable, "-c", _POOL_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "POOL-OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("levels,prequant", [(256, False), (64, False), (32, True)])
+def test_pinned_counts_early_band_d2h(engine, levels, prequant):
+    # several bands through the host pipeline into a PINNED counts buffer: the
+    # counts of band b go down (aux stream) while later bands still upload
+    import torch
+    w, h, nb = 2048, 2500, 3
+    imgs = [(tf.synth_noise if b % 2 == 0 else tf.synth_smooth)(w, h, 40 + b).pixels for b in range(nb)]
+    if prequant:
+        imgs = [((im.astype(np.uint32) * levels) >> 8).astype(np.uint8) for im in imgs]
+    dts = [(1, 0), (3, 45), (2, 90), (1, 135)]
+    cells = levels * levels
+    for pinned_in in (True, False):
+        src = np.concatenate(imgs)
+        if pinned_in:
+            src = torch.from_numpy(src).pin_memory().numpy()
+        out = torch.zeros(nb * len(dts) * cells, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+        got = engine.glcm(src, w, h, levels, dts, pixel_levels=levels if prequant else 256, n_bands=nb, out=out)
+        for b in range(nb):
+            for t, (d, a) in enumerate(dts):
+                want = (O.glcm_serial(imgs[b], w, h, levels, d, a) if prequant
+                        else O.glcm_gray(imgs[b], w, h, levels, d, a))
+                assert np.array_equal(got[b, t].reshape(-1), want), (pinned_in, b, d, a)
