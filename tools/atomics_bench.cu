@@ -20,11 +20,13 @@ enum Mode {
   M_SAME_ADDR_ADDN,         // same, variable increment
   M_LDS_STS_PRIVATE,        // non-atomic RMW, lane-private
   M_RANDOM_8WAY,            // COPIES8 layout: random cell*8 + lane%8 over 16K words
+  M_RANDOM_8WAY_RET,        // same, returning (what a drain check would need)
+  M_PACKED_16WAY_RET,       // L=64 candidate: 16 copies of packed u16 pairs, word*16 + lane%16, returning
   M_NMODES
 };
 const char* kNames[] = {"lane_private_inc", "lane_private_addn", "random_128KB_inc", "random_128KB_ret",
                         "random_16KB_inc", "same_addr_inc", "same_addr_addn", "lds_sts_private",
-                        "copies8_random"};
+                        "copies8_random", "copies8_random_ret", "packed16x16_random_ret"};
 
 template <int mode>
 __global__ void __launch_bounds__(kT, 1) bench(unsigned long long* cycles, uint32_t* sink) {
@@ -54,6 +56,10 @@ __global__ void __launch_bounds__(kT, 1) bench(unsigned long long* cycles, uint3
         break;
       }
       case M_RANDOM_8WAY: atomicAdd(&s[((r & 4095) << 3) | (lane & 7)], 1u); break;
+      case M_RANDOM_8WAY_RET: acc |= atomicAdd(&s[((r & 4095) << 3) | (lane & 7)], 1u); break;
+      case M_PACKED_16WAY_RET:
+        acc |= atomicAdd(&s[((r & 2047) << 4) | (lane & 15)], 1u << ((h >> 3) & 16));
+        break;
     }
   }
   const unsigned long long t1 = clock64();
@@ -116,7 +122,8 @@ int main() {
   cudaMalloc(&cyc, 8);
   cudaMalloc(&sink, 64);
   using K = void (*)(unsigned long long*, uint32_t*);
-  K ks[M_NMODES] = {bench<0>, bench<1>, bench<2>, bench<3>, bench<4>, bench<5>, bench<6>, bench<7>, bench<8>};
+  K ks[M_NMODES] = {bench<0>, bench<1>, bench<2>, bench<3>, bench<4>, bench<5>,
+                    bench<6>, bench<7>, bench<8>, bench<9>, bench<10>};
   for (auto k : ks) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
