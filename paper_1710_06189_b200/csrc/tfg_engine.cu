@@ -251,7 +251,8 @@ VoteKernel pick_global(int quant, int ksel) {
 }
 
 // Shared tail pool of the cooperative vote launches: per-band counters sit
-// 128 bytes past the grid-barrier counter (its own L2 line), in one memset.
+// 128 bytes past the grid-barrier counter (its own L2 line); all of them are
+// zeroed once and re-armed by each launch's last CTA.
 constexpr size_t kPoolCtrOffset = 32;
 constexpr int kMaxPoolBands = 1024;
 #ifndef TFG_POOL_PCT
@@ -472,10 +473,9 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   }
   dim3 grid((unsigned)per_band, (unsigned)n_bands);
   if (in_kernel_reduce) {
+    // counters are zero here: zeroed at context creation, re-armed by the
+    // last CTA of every cooperative launch (glcm_vote_kernel epilogue)
     p.sync_ctr = ctx->sync_ctr;
-    const size_t ctr_bytes = p.pool_ctr ? (kPoolCtrOffset + (size_t)n_bands) * sizeof(unsigned int)
-                                        : sizeof(unsigned int);
-    ck(cudaMemsetAsync(ctx->sync_ctr, 0, ctr_bytes, s), "memset");
     void* args[] = {&p};
     ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), grid, dim3(tfg::kThreads), args, smem, s),
        "glcm_vote_kernel cooperative launch");
@@ -756,6 +756,7 @@ int tfg_ctx_create(tfg_ctx** out, int device, unsigned flags) {
     ck(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ctx->band_ev, cudaEventDisableTiming), "event");
     ck(cudaMalloc(&ctx->sync_ctr, (kPoolCtrOffset + kMaxPoolBands) * sizeof(unsigned int)), "cudaMalloc");
+    ck(cudaMemset(ctx->sync_ctr, 0, (kPoolCtrOffset + kMaxPoolBands) * sizeof(unsigned int)), "memset");
   });
   if (rc != TFG_OK) {
     tfg_ctx_destroy(ctx);

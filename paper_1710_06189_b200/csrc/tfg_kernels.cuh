@@ -443,6 +443,10 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t 
 // Grid-wide barrier for a cooperative (co-resident) launch: every CTA has
 // stored its partial; thread 0 publishes arrival (release) and waits for all
 // `n` CTAs (acquire). The counter is zeroed by the host before the launch.
+// Counter words of a context's cooperative launches: [0] grid barrier,
+// [kExitCtr] CTAs done (re-arm), [32..] shared-pool counters per band.
+constexpr int kExitCtr = 16;
+
 __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int n) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -810,8 +814,20 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
       }
     }
     if (p.sync_ctr) {
-      grid_barrier(p.sync_ctr, gridDim.x * gridDim.y);
+      const unsigned int n = gridDim.x * gridDim.y;
+      grid_barrier(p.sync_ctr, n);
       reduce_partials_slice<STRAT == S_PACKED16>(p, hist, band_idx, glcm);
+      // The last CTA out re-arms the counters for the next launch on the
+      // stream (every CTA has left the barrier spin and the pool by now), so
+      // the host needs no memset per launch.
+      if (threadIdx.x == 0) {
+        if (atomicAdd(p.sync_ctr + kExitCtr, 1u) == n - 1) {
+          *reinterpret_cast<volatile unsigned int*>(p.sync_ctr) = 0u;
+          *reinterpret_cast<volatile unsigned int*>(p.sync_ctr + kExitCtr) = 0u;
+          if (p.pool_ctr)
+            for (unsigned int b = 0; b < gridDim.y; ++b) reinterpret_cast<volatile unsigned int*>(p.pool_ctr)[b] = 0u;
+        }
+      }
     }
     return;
   }
