@@ -65,7 +65,6 @@ WORKLOADS = {
     "t5": dict(width=4096, height=4096, levels=(64,), ds=(1,), kinds=("noise",), layout="rows-strong", bands=1),
     "t4": dict(width=1024, height=1024, levels=(32,), ds=(1,), kinds=("noise",), layout="bands", bands=10),
 }
-GEN_BLOCK = 1024  # rows per generator block of the strong-scaling images (content independent of N)
 
 
 def log(*a):
@@ -179,10 +178,21 @@ def noise_pixels(tf, width, height, seed):
 _GEN_ENGINES = {}
 
 
-def gen_rows(tf, kind, width, row0, rows, block_rows, seed0):
-    """Rows [row0, row0+rows) of an image made of generator blocks of
-    `block_rows` rows, block b = synth_<kind>(width, block_rows, seed0 + b).
-    The content does not depend on how the rows are later partitioned."""
+def gen_rows(tf, kind, width, row0, rows, block_rows, seed0, height=None):
+    """Rows [row0, row0+rows) of the workload image. block_rows=None: the one
+    image synth_<kind>(width, height, seed0) (rows-strong; noise rows come
+    straight from the device generator jumped to output row0*width). Else an
+    image of generator blocks of `block_rows` rows, block b =
+    synth_<kind>(width, block_rows, seed0 + b) (rows-weak). The content does
+    not depend on how the rows are later partitioned."""
+    if block_rows is None:
+        import torch
+        if kind == "noise" and torch.cuda.is_available():
+            dev = torch.cuda.current_device()
+            eng = _GEN_ENGINES.get(dev) or _GEN_ENGINES.setdefault(dev, tf.Engine(dev))
+            return eng.synth_noise_rows_device(width, row0, rows, seed0).cpu().numpy()
+        full = (tf.synth_noise if kind == "noise" else tf.synth_smooth)(width, height, seed0).pixels
+        return full[row0 * width:(row0 + rows) * width].copy()
     out = np.empty(rows * width, dtype=np.uint8)
     r = row0
     while r < row0 + rows:
@@ -210,7 +220,8 @@ class Plan:
         self.dts = [(d, a) for d in cfg["ds"] for a in angles]
         self.kinds = cfg["kinds"]
         self.layout = cfg["layout"]
-        self.halo = D.halo_rows(self.dts) if self.layout.startswith("rows") else 0
+        # rows of halo below a shard (pipeline.hpp:60-61: d for the downward angles, none at 0 degrees)
+        self.halo = max([d for d, a in self.dts if a != 0], default=0) if self.layout.startswith("rows") else 0
         self.bands = 1
         if self.layout == "rows-weak":
             self.height = cfg["block_rows"] * world          # global image
@@ -222,10 +233,12 @@ class Plan:
                 if world > 1 else None
             self.owned0 = spec.owned_row_start if spec else 0
             self.owned = spec.owned_rows() if spec else self.height
-            self.gen_block = GEN_BLOCK
+            self.gen_block = None  # one synth image, BASELINE config 5
         elif self.layout == "bands":
             self.height = cfg["height"]
-            self.band_ids = list(D.bands_for_rank(cfg["bands"], world, rank))
+            base, extra = divmod(cfg["bands"], world)  # contiguous blocks (distributed.bands_for_rank)
+            start = rank * base + min(rank, extra)
+            self.band_ids = list(range(start, start + base + (1 if rank < extra else 0)))
             self.bands = len(self.band_ids)
             self.owned0, self.owned = 0, self.height
         else:  # replica
@@ -280,7 +293,7 @@ def make_host_inputs(plan, tf):
             imgs[kind] = np.concatenate([noise_pixels(tf, plan.width, plan.height, b + 1)
                                          for b in plan.band_ids])
         elif plan.layout.startswith("rows"):
-            imgs[kind] = gen_rows(tf, kind, plan.width, plan.owned0, plan.owned, plan.gen_block, 1)
+            imgs[kind] = gen_rows(tf, kind, plan.width, plan.owned0, plan.owned, plan.gen_block, 1, plan.height)
         elif kind == "noise":
             imgs[kind] = noise_pixels(tf, plan.width, plan.height, 1)
         else:
@@ -302,56 +315,80 @@ def ref_image(r, gray, w, h, L):
     return hd
 
 
+def ref_synth(r, kind, w, h, seed):
+    """The reference's own synth_noise / synth_smooth (image.hpp:76-116)."""
+    out = np.empty(w * h, dtype=np.uint8)
+    fn = r.ref_synth_noise if kind == "noise" else r.ref_synth_smooth
+    if fn(w, h, seed, out.ctypes.data_as(C.POINTER(C.c_uint8))):
+        raise RuntimeError("reference synth failed")
+    return out
+
+
 def run_reference(args, wl):
+    """The reference's own CPU path on this box's host cores, nothing of the
+    engine loaded: inputs from the reference's generators, its quantize, and
+    compute_glcm_privatized (parallel.hpp:240-254) on all host threads for
+    every (input, L, d, theta) GLCM of one step of the workload."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import oracle as O
-    from paper_1710_06189_b200 import distributed as D
-    from paper_1710_06189_b200 import texforge as tf
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtexforge_ref.so not built"}))
         return
-    plan = Plan(wl, 1, 0, tf, D)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    plan = Plan(wl, 1, 0, None, None)
     threads = os.cpu_count() or 1
-    w = plan.width
-    h = plan.height if plan.layout != "rows-weak" else plan.cfg["block_rows"]
-    if plan.layout == "rows-strong":
-        h = min(h, 8192)  # bounded sample: the first 8192 rows of the 65536^2 image
     r = O.ref()
-    imgs = {}
+    w = plan.width
+    t0 = time.time()
+    if plan.layout == "rows-weak":
+        h, units = plan.cfg["block_rows"], [1]  # one generator block (seed 1); N blocks = N x the same work
+    elif plan.layout == "bands":
+        h, units = plan.height, [b + 1 for b in range(plan.cfg["bands"])]
+    else:
+        h, units = plan.height, [1]
+    handles = {}
     for kind in plan.kinds:
-        gen = tf.synth_noise if kind == "noise" else tf.synth_smooth
-        imgs[kind] = gen(w, h, 1).pixels
-    jobs = [(k, L, d, a) for L in plan.levels_list for (d, a) in plan.dts for k in plan.kinds]
-    handles = {(k, L): ref_image(r, imgs[k][: w * h], w, h, L) for k in plan.kinds for L in plan.levels_list}
+        for u in units:
+            gray = ref_synth(r, kind, w, h, u)
+            for L in plan.levels_list:
+                handles[(kind, u, L)] = ref_image(r, gray, w, h, L)
+            del gray
+    log(f"[reference] inputs ready in {time.time() - t0:.1f}s")
+    jobs = [(k, u, L, d, a) for L in plan.levels_list for k in plan.kinds for u in units for (d, a) in plan.dts]
     outs = {L: np.zeros(L * L, dtype=np.uint64) for L in plan.levels_list}
-    per_step = min(len(jobs), 2)
 
-    def step(s):
+    def step():
         p = 0
-        for j in range(per_step):
-            kind, L, d, a = jobs[(s * per_step + j) % len(jobs)]
-            assert r.ref_image_glcm(handles[(kind, L)], d, a, threads, 1,
-                                    outs[L].ctypes.data_as(C.POINTER(C.c_uint64))) == 0
+        for kind, u, L, d, a in jobs:
+            if r.ref_image_glcm(handles[(kind, u, L)], d, a, threads, 1,
+                                outs[L].ctypes.data_as(C.POINTER(C.c_uint64))):
+                raise RuntimeError("reference compute_glcm_privatized failed")
             p += valid_pairs(w, h, d, a)
         return p
 
-    for s in range(args.warmup):
-        step(s)
+    for _ in range(args.warmup):
+        step()
     t = time.perf_counter()
-    pairs = sum(step(args.warmup + s) for s in range(args.steps))
+    pairs = sum(step() for _ in range(args.steps))
     el = time.perf_counter() - t
     v = pairs / el / 1e9
-    sample = (f"{per_step} GLCMs/step, rotating over {len(jobs)} (input, L, d, theta) jobs, of {w}x{h} images; "
-              f"reference compute_glcm_privatized (unmodified headers), {threads} workers")
+    n_img = len(units) * len(plan.kinds)
+    sample = (f"every GLCM of one step: {len(jobs)} (input, L, d, theta) jobs over {n_img} {w}x{h} image(s)"
+              + (f" (one of the {world} row blocks a step covers at N={world}; each block is the same work)"
+                 if plan.layout == "rows-weak" and world > 1 else "")
+              + f"; reference compute_glcm_privatized (unmodified headers), {threads} workers")
     for hd in handles.values():
         r.ref_image_free(hd)
     print(json.dumps({
-        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
-        "scaling": plan.scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic", "impl": "reference",
-        "config": {"workload": plan.describe(), "host_threads": threads},
+        "scaling": Plan(wl, world, 0, None, None).scaling if plan.layout != "rows-strong" else "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference synth_noise / synth_smooth)",
+        "impl": "reference",
+        "config": {"workload": Plan(wl, 1, 0, None, None).describe(), "host_threads": threads,
+                   "pairs_per_step": pairs // args.steps, "glcms_per_step": len(jobs)},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -385,6 +422,59 @@ def cpu_baseline(plan, imgs, seconds, threads):
                       f"compute_glcm_privatized, unmodified headers, {threads} workers, ~{seconds:.0f}s)"}
 
 
+# --------------------------------------------------------------------------- correctness gate
+def golden_for(plan):
+    """{(kind, L, d, theta): fnv} of the reference's own GLCMs of this plan's
+    GLOBAL image, where tests/golden holds them."""
+    out = {}
+    gdir = os.path.join(ROOT, "tests", "golden")
+    if plan.wl in ("c3", "c1", "c2", "c5"):
+        with open(os.path.join(gdir, "golden_hashes.json")) as f:
+            small = json.load(f)["glcm"]
+        if plan.layout != "rows-weak" or plan.world == 1:
+            for g in small:
+                if g["size"] == plan.width and g["size"] == plan.height and g.get("seed", 1) == 1:
+                    out[(g["kind"], g["levels"], g["d"], g["theta"])] = g["fnv"]
+    try:
+        with open(os.path.join(gdir, "golden_large.json")) as f:
+            large = json.load(f)
+    except OSError:
+        return out
+    if plan.wl == "c5":
+        for g in large.get("c5", []):
+            out[(g["kind"], g["levels"], g["d"], g["theta"])] = g["fnv"]
+    if plan.wl == "c3" and plan.world == 1:
+        for g in large.get("c3_smooth_d", []):
+            out[(g["kind"], g["levels"], g["d"], g["theta"])] = g["fnv"]
+    if plan.wl == "c3" and plan.world > 1:
+        for g in large.get("c3_blocks", []):
+            if g["blocks"] == plan.world:
+                out[(g["kind"], g["levels"], g["d"], g["theta"])] = g["fnv"]
+    return out
+
+
+def single_gpu_recompute(plan, tf, eng, lib, jobs, out_off, cells, reduced):
+    """Rank 0: the global image of a row-partitioned plan on this one GPU,
+    voted with the N=1 path; returns how many reduced GLCMs equal it."""
+    import torch
+    from paper_1710_06189_b200 import _lib as Lb
+    W, H = plan.width, plan.height
+    want = torch.zeros(reduced.size, dtype=torch.int64, device="cuda")
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for kind in plan.kinds:
+        img = torch.from_numpy(gen_rows(tf, kind, W, 0, H, plan.gen_block, 1, H)).cuda()
+        for j, (L, k, d, a) in enumerate(jobs):
+            if k != kind:
+                continue
+            Lb.check(lib.tfg_glcm_async(eng.handle, C.c_void_p(img.data_ptr()), W, H, W, H, 256, L, d, a, 0,
+                                        C.c_void_p(want.data_ptr() + out_off[j] * 8), s))
+        torch.cuda.synchronize()
+        del img
+    want = want.cpu().numpy().view(np.uint64)
+    return sum(int(np.array_equal(reduced[out_off[j]:out_off[j] + cells[L]], want[out_off[j]:out_off[j] + cells[L]]))
+               for j, (L, _k, _d, _a) in enumerate(jobs))
+
+
 # --------------------------------------------------------------------------- engine arm
 def run_engine(args, wl):
     import torch
@@ -404,6 +494,9 @@ def run_engine(args, wl):
     dist = None
     if world > 1:
         import torch.distributed as dist
+        if backend == "nccl" and torch.cuda.device_count() < world:
+            raise SystemExit(f"bench: {world} ranks need {world} GPUs for NCCL, this box has "
+                             f"{torch.cuda.device_count()} (TFG_DIST_BACKEND=gloo runs the N>1 logic on one GPU)")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -502,8 +595,13 @@ def run_engine(args, wl):
         if dist is not None and plan.layout.startswith("rows"):
             D.reduce_sum_(acc)  # ONE NCCL reduce of every partial GLCM
 
-    # correctness gate (first step, untimed): conservation on every GLCM, and
-    # the reference-generated Appendix-A hashes where the workload has them
+    # correctness gate (first step, untimed, rank 0 after the reduce):
+    #  * conservation: every GLCM sums to valid_pair_count of the global image;
+    #  * golden: the reference's own FNV-1a hashes of the same global image
+    #    (tests/golden: Appendix A, golden_large.json for c5 and the N-block c3);
+    #  * at N > 1, a single-GPU recompute: rank 0 builds the whole global image
+    #    and votes it with the N=1 path (golden-pinned), and every reduced GLCM
+    #    must equal it bit for bit (catches halo / ownership / reduce errors).
     step()
     torch.cuda.synchronize()
     check = {"conservation": None, "golden": None}
@@ -515,18 +613,37 @@ def run_engine(args, wl):
                 seg = host[out_off[j] + b * cells[L]: out_off[j] + (b + 1) * cells[L]]
                 ok &= int(seg.sum()) == valid_pairs(W, plan.height, d, a)
         check["conservation"] = bool(ok)
-        if wl == "c3" and world == 1:
-            with open(os.path.join(ROOT, "tests", "golden", "golden_hashes.json")) as f:
-                gold = {(g["kind"], g["size"], g["levels"], g["d"], g["theta"]): g["fnv"]
-                        for g in json.load(f)["glcm"]}
+        gold = golden_for(plan)
+        if gold:
             n_ok = n_all = 0
             for j, (L, kind, d, a) in enumerate(jobs):
-                key = (kind, W, L, d, a)
-                if key in gold and d == 1:
+                key = (kind, L, d, a)
+                if key in gold:
                     n_all += 1
                     n_ok += fnv1a64(host[out_off[j]: out_off[j] + cells[L]]) == gold[key]
-            check["golden"] = f"{n_ok}/{n_all} Appendix-A FNV-1a hashes match"
+            check["golden"] = f"{n_ok}/{n_all} reference FNV-1a hashes of the global image match"
             ok &= n_ok == n_all
+        if plan.layout == "bands":
+            with open(os.path.join(ROOT, "tests", "golden", "golden_hashes.json")) as f:
+                gb = {(g["kind"], g["seed"], g["levels"], g["d"], g["theta"]): g["fnv"]
+                      for g in json.load(f)["glcm"] if g["size"] == W == plan.height}
+            n_ok = n_all = 0
+            for j, (L, kind, d, a) in enumerate(jobs):
+                for b, band in enumerate(plan.band_ids):
+                    key = (kind, band + 1, L, d, a)
+                    if key in gb:
+                        n_all += 1
+                        seg = host[out_off[j] + b * cells[L]: out_off[j] + (b + 1) * cells[L]]
+                        n_ok += fnv1a64(seg) == gb[key]
+            check["golden"] = f"{n_ok}/{n_all} reference FNV-1a hashes of this rank's bands match"
+            ok &= n_ok == n_all
+        if world > 1 and plan.layout.startswith("rows"):
+            same = single_gpu_recompute(plan, tf, eng, lib, jobs, out_off, cells, host)
+            check["single_gpu_recompute"] = f"{same}/{len(jobs)} GLCMs equal the whole image voted on one GPU"
+            ok &= same == len(jobs)
+        if os.environ.get("TFG_BENCH_DUMP"):  # tests: the gated GLCMs, for an independent oracle check
+            np.savez(os.environ["TFG_BENCH_DUMP"], counts=host, offsets=np.array(out_off),
+                     jobs=np.array([(L, plan.kinds.index(k), d, a) for (L, k, d, a) in jobs]))
         if not ok:
             raise SystemExit(f"bench correctness gate failed: {check}")
     for _ in range(args.warmup):
@@ -741,6 +858,19 @@ def main():
     if args.warmup < 3:
         log("note: warmup raised to the contract minimum of 3")
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.run(cmd).returncode)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, args.workload)
     else:

@@ -128,6 +128,13 @@ int tfg_synth_noise_parallel(size_t n, uint32_t seed, uint8_t* out, int threads)
 int tfg_synth_noise_device(tfg_ctx* ctx, size_t width, size_t height, uint32_t seed, uint8_t* d_out,
                            size_t pitch, void* stream);
 
+/* Rows [row0, row0 + rows) of synth_noise(width, <any height>, seed) on the
+ * device (pixel (y, x) of those rows -> d_out[(y - row0)*pitch + x]): the
+ * generator jumps straight to output row0*width, so a GPU of a row-partitioned
+ * image makes only its own shard. Returns after the kernel has finished. */
+int tfg_synth_noise_rows_device(tfg_ctx* ctx, size_t width, size_t row0, size_t rows, uint32_t seed,
+                                uint8_t* d_out, size_t pitch, void* stream);
+
 /* ---- the hot path ---------------------------------------------------------- */
 
 /* quantize (image.hpp:55-62) on the device; gray/out host or device per flags */
@@ -233,6 +240,63 @@ int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
 /* Device post-processing on `stream`: symmetrize (in place allowed? no: out != in). */
 int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned flags,
                    uint64_t* d_sym_out, double* d_probs_out, double* d_feats_out, void* stream);
+
+/* ---- multi-GPU ---------------------------------------------
+ * One process, n GPUs: a group of engine contexts plus one NCCL communicator
+ * over them (ncclCommInitAll; NVLink/NVSwitch on a B200 box). Failures of a
+ * collective return TFG_COLLECTIVE_ERROR. */
+typedef struct tfg_group tfg_group;
+
+/* devices: n_gpus CUDA ordinals, or NULL for 0..n_gpus-1. */
+int tfg_group_create(tfg_group** out, int n_gpus, const int* devices, unsigned flags);
+void tfg_group_destroy(tfg_group* g);
+int tfg_group_size(const tfg_group* g);
+tfg_ctx* tfg_group_ctx(tfg_group* g, int i);
+uint64_t tfg_group_launch_count(tfg_group* g);
+
+/* One host image row-partitioned over the group: partition(W, H, p, G)
+ * (R/include/texforge/pipeline.hpp:48-73) gives GPU g its owned rows plus the
+ * d-row halo, which it streams through its own Scheme-3 copy/vote pipeline,
+ * voting only its owned anchors; the partial GLCMs are summed with ONE
+ * ncclReduce into GPU 0 (exact integer sums, like merge_chunk_glcms,
+ * pipeline.hpp:231-240), then post-processed there. Same outputs and errors
+ * as tfg_glcm (which replaces compute_glcm_serial, glcm.hpp:144). */
+int tfg_group_glcm(tfg_group* g, const uint8_t* px, size_t width, size_t height, int pixel_levels, int levels,
+                   const int* distances, const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out,
+                   double* probs_out, double* feats_out);
+
+/* Multispectral batch sharded over the group: contiguous blocks of bands per
+ * GPU, no collective (each GPU writes its own bands' results). Same layout as
+ * tfg_glcm_bands. */
+int tfg_group_glcm_bands(tfg_group* g, const uint8_t* px, size_t width, size_t height, size_t band_stride,
+                         size_t n_bands, int pixel_levels, int levels, const int* distances, const int* angles_deg,
+                         int n_dt, unsigned flags, uint64_t* counts_out, double* probs_out, double* feats_out);
+
+/* Scheme 3 over the group (compute_glcm_chunked, pipeline.hpp:246-337): chunk i
+ * of partition(W, H, p, K) runs on GPU floor(i*G/K); `fetch` calls are
+ * serialised (never concurrent); one ncclReduce. A fetch failure returns
+ * TFG_SOURCE_ERROR with tfg_last_error_chunk() = the chunk index. */
+int tfg_group_glcm_chunked(tfg_group* g, size_t width, size_t height, int pixel_levels, int levels,
+                           const int* distances, const int* angles_deg, int n_dt, size_t chunk_count,
+                           tfg_fetch_fn fetch, void* user, unsigned flags, uint64_t* counts_out, double* probs_out,
+                           double* feats_out);
+
+/* One process per GPU (torchrun-style): a rank's NCCL communicator. */
+typedef struct tfg_comm tfg_comm;
+#define TFG_COMM_ID_BYTES 128
+/* ncclGetUniqueId on the root rank; the caller ships the bytes to every rank. */
+int tfg_comm_unique_id(uint8_t* id /* TFG_COMM_ID_BYTES */);
+int tfg_comm_init_rank(tfg_comm** out, tfg_ctx* ctx, int nranks, int rank, const uint8_t* id);
+void tfg_comm_destroy(tfg_comm* c);
+/* In-place SUM of n u64 device counts onto `root` (one ncclReduce on `stream`). */
+int tfg_comm_reduce_counts(tfg_comm* c, uint64_t* d_counts, size_t n, int root, void* stream);
+/* Row-partition halo (pipeline.hpp:60-61): rank r sends its first `halo` rows
+ * of d_slab to rank r-1 and receives rank r+1's first `halo` rows into rows
+ * [owned_rows, owned_rows + halo) of its own slab (ncclSend/ncclRecv). */
+int tfg_comm_exchange_halo(tfg_comm* c, uint8_t* d_slab, size_t pitch, size_t owned_rows, size_t halo,
+                           void* stream);
+/* In-place MAX all-reduce of n f64 (timing: the slowest rank defines a step). */
+int tfg_comm_allreduce_max_f64(tfg_comm* c, double* d_vals, size_t n, void* stream);
 
 /* Device error flag accumulated by *_async calls (non-zero = a quantised input held a
  * value >= levels); reading it synchronises the context's streams and clears it. */

@@ -63,6 +63,7 @@ SIGNATURES = [
     ("tfg_mt19937_windows", C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, _sz, C.POINTER(C.c_uint32), C.c_int]),
     ("tfg_synth_noise_parallel", C.c_int, [_sz, C.c_uint32, _u8p, C.c_int]),
     ("tfg_synth_noise_device", C.c_int, [C.c_void_p, _sz, _sz, C.c_uint32, C.c_void_p, _sz, C.c_void_p]),
+    ("tfg_synth_noise_rows_device", C.c_int, [C.c_void_p, _sz, _sz, _sz, C.c_uint32, C.c_void_p, _sz, C.c_void_p]),
     ("tfg_quantize", C.c_int, [C.c_void_p, C.c_void_p, _sz, C.c_int, C.c_void_p, C.c_uint]),
     ("tfg_glcm", C.c_int, [C.c_void_p, C.c_void_p, _sz, _sz, _sz, C.c_int, C.c_int, _ip, _ip, C.c_int,
                            C.c_uint, _u64p, _dp, _dp]),

@@ -120,8 +120,15 @@ struct tfg_ctx {
   DevBuf partials;                       // per-CTA sub-GLCMs (large L)
   DevBuf qbuf;                           // quantize in/out
   DevBuf tmp;                            // per-(d,theta) band scratch
-  int* d_err = nullptr;                  // async error flag (+ per-GLCM flags)
+  int* d_err = nullptr;                  // [0] async validation flag, [1]/[2] async post flags, [kSyncErr] sync calls
   unsigned int* sync_ctr = nullptr;      // grid-barrier counter of the cooperative vote launches
+  // Launches with per-CTA partials (L > 64) share `partials` and the
+  // cooperative counters: each one waits for the previous one (on whatever
+  // stream it ran) through this event, so two streams or a sync call plus an
+  // async call never overlap on the shared scratch.
+  cudaEvent_t scratch_ev = nullptr;
+  cudaStream_t scratch_stream = nullptr;
+  bool scratch_used = false;
   DevBuf errs;
   HostBuf hout;                          // pinned result staging
   std::atomic<uint64_t> launches{0};
@@ -129,6 +136,9 @@ struct tfg_ctx {
 };
 
 namespace {
+
+constexpr int kSyncErr = 3;  // d_err word of the synchronous calls' validation
+int* sync_err(tfg_ctx* ctx) { return ctx->d_err + kSyncErr; }
 
 struct DeviceGuard {
   int prev = -1;
@@ -398,6 +408,37 @@ int quant_mode(int pixel_levels, int levels, uint32_t* mask, int* shift, int* lg
   return tfg::Q_MUL;
 }
 
+// Orders the launches that share the context's per-CTA partials and
+// cooperative counters (L > 64): the launch on `s` first waits for the
+// previous such launch when that ran on another stream, and records the
+// event for the next one when it goes out of scope. Skipped while `s` is
+// being captured into a CUDA graph (the graph itself fixes the order).
+struct ScratchOrder {
+  tfg_ctx* ctx;
+  cudaStream_t s;
+  bool on;
+  ScratchOrder(tfg_ctx* c, cudaStream_t st, bool use) : ctx(c), s(st), on(use) {
+    if (!on) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      on = false;
+      return;
+    }
+    if (ctx->scratch_used && ctx->scratch_stream != s)
+      ck(cudaStreamWaitEvent(s, ctx->scratch_ev, 0), "wait scratch");
+  }
+  ~ScratchOrder() {
+    if (!on) return;
+    if (cudaEventRecord(ctx->scratch_ev, s) == cudaSuccess) {
+      ctx->scratch_stream = s;
+      ctx->scratch_used = true;
+    } else {
+      cudaGetLastError();
+    }
+  }
+};
+
 // Enqueue the vote of one (d, theta) for n_bands bands into d_glcm (added).
 void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
                  size_t band_stride, int n_bands, size_t row_end, int pixel_levels, int levels,
@@ -466,6 +507,7 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   p.main_per_cta = ((p.pool_beg + per_band - 1) / per_band + 63) / 64 * 64;
   p.edge_per_cta = (p.edge_items + per_band - 1) / per_band;
   const bool packed_partials = use_partials && strat == tfg::S_PACKED16;
+  ScratchOrder order(ctx, s, use_partials);
   if (use_partials) {
     const size_t per_cta = packed_partials ? words : cells;
     const size_t bytes = (size_t)per_band * n_bands * per_cta * 4;
@@ -477,8 +519,15 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
     // last CTA of every cooperative launch (glcm_vote_kernel epilogue)
     p.sync_ctr = ctx->sync_ctr;
     void* args[] = {&p};
-    ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), grid, dim3(tfg::kThreads), args, smem, s),
-       "glcm_vote_kernel cooperative launch");
+    const cudaError_t e =
+        cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), grid, dim3(tfg::kThreads), args, smem, s);
+    if (e != cudaSuccess) {
+      // a launch that did not run leaves the counters as they were; re-zero
+      // them anyway so no later launch can spin on a stale arrival count
+      cudaGetLastError();
+      cudaMemsetAsync(ctx->sync_ctr, 0, (kPoolCtrOffset + kMaxPoolBands) * sizeof(unsigned int), s);
+      ck(e, "glcm_vote_kernel cooperative launch");
+    }
     ctx->launches++;
     return;
   }
@@ -609,14 +658,17 @@ void finish(tfg_ctx* ctx, unsigned long long* d_counts, int n, int levels, unsig
   if (feats_out && b_feats) std::memcpy(feats_out, h + b_counts + b_probs, b_feats);
 }
 
-void check_async_flag(tfg_ctx* ctx, cudaStream_t s) {
+// The synchronous calls validate pre-quantised input into their own error
+// word (d_err[kSyncErr], zeroed on the call's stream before its first
+// validation); d_err[0] belongs to the *_async API and tfg_check_async_errors.
+void clear_sync_flag(tfg_ctx* ctx, cudaStream_t s) {
+  ck(cudaMemsetAsync(sync_err(ctx), 0, sizeof(int), s), "memset");
+}
+void check_sync_flag(tfg_ctx* ctx, cudaStream_t s) {
   int flag = 0;
-  ck(cudaMemcpyAsync(&flag, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H err");
+  ck(cudaMemcpyAsync(&flag, sync_err(ctx), sizeof(int), cudaMemcpyDeviceToHost, s), "D2H err");
   ck(cudaStreamSynchronize(s), "stream sync");
-  if (flag) {
-    ck(cudaMemset(ctx->d_err, 0, sizeof(int)), "memset");
-    fail(TFG_INVALID_ARGUMENT, "QuantizedImage: pixel value exceeds gray level");
-  }
+  if (flag) fail(TFG_INVALID_ARGUMENT, "QuantizedImage: pixel value exceeds gray level");
 }
 
 // Host copy split over up to 16 host threads (pageable -> pinned staging).
@@ -678,14 +730,16 @@ std::vector<uint64_t> chunk_specs(size_t width, size_t height, const int* distan
 // Scheme 3 pipeline over host rows. `fetch_rows(i, start, end, dst_host_or_null)`
 // either fills a pinned slot (returns that pointer) or returns a pointer to
 // the caller's own host rows.
+// `specs`: k chunks {owned_row_start, owned_row_end, buffer_row_end} (any
+// subset of a partition(): a GPU of a multi-GPU group runs its own chunks).
 template <typename Fetch>
-void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, int levels,
-                  const int* distances, const int* angles, int n_dt, size_t k, unsigned flags,
-                  unsigned long long* d_acc, Fetch&& fetch_rows, size_t total_rows = 0, size_t n_bands = 1,
-                  size_t acc_band_stride = 0, const std::function<void(size_t)>& band_done = nullptr) {
+void run_pipeline_specs(tfg_ctx* ctx, size_t width, const std::vector<uint64_t>& specs, int pixel_levels,
+                        int levels, const int* distances, const int* angles, int n_dt, unsigned flags,
+                        unsigned long long* d_acc, Fetch&& fetch_rows, size_t n_bands = 1,
+                        size_t acc_band_stride = 0, const std::function<void(size_t)>& band_done = nullptr) {
   // The ring runs continuously over (band, chunk): band b+1's first copy
   // overlaps band b's last votes. Band b's GLCMs go to d_acc + b*acc_band_stride.
-  const std::vector<uint64_t> specs = chunk_specs(width, height, distances, angles, n_dt, k, total_rows);
+  const size_t k = specs.size() / 3;
   const size_t pitch = round16(width);
   size_t max_rows = 0;
   for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, specs[3 * i + 2] - specs[3 * i]);
@@ -705,7 +759,7 @@ void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, i
     ck(cudaMemcpy2DAsync(dst, pitch, src, width, width, rows, cudaMemcpyHostToDevice, ctx->copy), "H2D chunk");
     ck(cudaEventRecord(ctx->copied[sl], ctx->copy), "event record");
     ck(cudaStreamWaitEvent(ctx->exec, ctx->copied[sl], 0), "wait");
-    if (pixel_levels == levels) launch_validate(ctx, dst, width, rows, pitch, 0, 1, levels, ctx->d_err, ctx->exec);
+    if (pixel_levels == levels) launch_validate(ctx, dst, width, rows, pitch, 0, 1, levels, sync_err(ctx), ctx->exec);
     for (int t = 0; t < n_dt; ++t)
       launch_vote(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, levels, distances[t],
                   angles[t], flags, d_acc + bnd * acc_band_stride + (size_t)t * levels * levels, ctx->exec);
@@ -713,6 +767,50 @@ void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, i
     if (band_done && i == k - 1) band_done(bnd);
     if (sequential) ck(cudaStreamSynchronize(ctx->exec), "stream sync");
   }
+}
+
+template <typename Fetch>
+void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, int levels,
+                  const int* distances, const int* angles, int n_dt, size_t k, unsigned flags,
+                  unsigned long long* d_acc, Fetch&& fetch_rows, size_t total_rows = 0, size_t n_bands = 1,
+                  size_t acc_band_stride = 0, const std::function<void(size_t)>& band_done = nullptr) {
+  run_pipeline_specs(ctx, width, chunk_specs(width, height, distances, angles, n_dt, k, total_rows), pixel_levels,
+                     levels, distances, angles, n_dt, flags, d_acc, std::forward<Fetch>(fetch_rows), n_bands,
+                     acc_band_stride, band_done);
+}
+
+// Host image(s) -> the Scheme-3 stream pipeline over (band, chunk), votes
+// added into d_acc ([band][dt][cell]): copy chunk n+1 while voting chunk n,
+// across band boundaries. `height` buffer rows of which anchors in rows
+// [0, owned_rows) vote. Pinned caller memory is DMA'd in place; pageable
+// memory would make every cudaMemcpyAsync a synchronous bounce-buffer copy,
+// so its rows are first copied (by several host threads) into the pinned
+// ring slot. `band_done(b)`: called once band b's last votes are enqueued.
+void host_vote(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t owned_rows, size_t band_stride,
+               size_t n_bands, int pixel_levels, int levels, const int* distances, const int* angles_deg, int n_dt,
+               unsigned flags, unsigned long long* d_acc,
+               const std::function<void(size_t)>& band_done = nullptr) {
+  int dmax = 1;
+  for (int i = 0; i < n_dt; ++i) dmax = std::max(dmax, distances[i]);
+  const size_t k = auto_chunks(width, owned_rows, dmax);
+  const bool pageable = host_memory_kind(px) == 0;
+  if (pageable) {
+    const std::vector<uint64_t> sp = chunk_specs(width, owned_rows, distances, angles_deg, n_dt, k, height);
+    size_t max_rows = 0;
+    for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, sp[3 * i + 2] - sp[3 * i]);
+    for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->hslot[sl].get(max_rows * width + 64);
+  }
+  const size_t band_words = (size_t)n_dt * levels * levels;
+  run_pipeline(
+      ctx, width, owned_rows, pixel_levels, levels, distances, angles_deg, n_dt, k, flags, d_acc,
+      [&](size_t b, size_t, size_t start, size_t, size_t buf_end, int sl) -> const uint8_t* {
+        const uint8_t* src = px + b * band_stride + start * width;
+        if (!pageable) return src;
+        uint8_t* dst = static_cast<uint8_t*>(ctx->hslot[sl].p);
+        parallel_memcpy(dst, src, (buf_end - start) * width);
+        return dst;
+      },
+      height, n_bands, band_words, band_done);
 }
 
 }  // namespace
@@ -748,7 +846,8 @@ int tfg_ctx_create(tfg_ctx** out, int device, unsigned flags) {
       ck(cudaEventCreateWithFlags(&ctx->consumed[i], cudaEventDisableTiming), "event");
     }
     ck(cudaMalloc(&ctx->d_err, 64), "cudaMalloc");
-    ck(cudaMemset(ctx->d_err, 0, 64), "memset");
+    ck(cudaMemsetAsync(ctx->d_err, 0, 64, ctx->exec), "memset");
+    ck(cudaEventCreateWithFlags(&ctx->scratch_ev, cudaEventDisableTiming), "event");
     for (int i = 0; i < tfg_ctx::kAux; ++i) {
       ck(cudaStreamCreateWithFlags(&ctx->aux[i], cudaStreamNonBlocking), "stream");
       ck(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming), "event");
@@ -756,7 +855,11 @@ int tfg_ctx_create(tfg_ctx** out, int device, unsigned flags) {
     ck(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ctx->band_ev, cudaEventDisableTiming), "event");
     ck(cudaMalloc(&ctx->sync_ctr, (kPoolCtrOffset + kMaxPoolBands) * sizeof(unsigned int)), "cudaMalloc");
-    ck(cudaMemset(ctx->sync_ctr, 0, (kPoolCtrOffset + kMaxPoolBands) * sizeof(unsigned int)), "memset");
+    ck(cudaMemsetAsync(ctx->sync_ctr, 0, (kPoolCtrOffset + kMaxPoolBands) * sizeof(unsigned int), ctx->exec),
+       "memset");
+    // every stream of the context is non-blocking: finish the zeroing before
+    // any launch on another stream can read the counters
+    ck(cudaStreamSynchronize(ctx->exec), "stream sync");
   });
   if (rc != TFG_OK) {
     tfg_ctx_destroy(ctx);
@@ -797,6 +900,7 @@ void tfg_ctx_destroy(tfg_ctx* ctx) {
       if (ctx->join_ev[i]) cudaEventDestroy(ctx->join_ev[i]);
     }
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->scratch_ev) cudaEventDestroy(ctx->scratch_ev);
     if (ctx->band_ev) cudaEventDestroy(ctx->band_ev);
     if (ctx->exec) cudaStreamDestroy(ctx->exec);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
@@ -896,12 +1000,11 @@ int tfg_quantize(tfg_ctx* ctx, const uint8_t* gray, size_t n, int levels, uint8_
 namespace {
 // One image (or n_bands images) of `height` buffer rows whose anchors in rows
 // [0, owned_rows) vote (owned_rows == height: the whole image).
-int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t owned_rows, size_t pitch,
-              size_t band_stride, size_t n_bands, int pixel_levels, int levels, const int* distances,
-              const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out, double* probs_out,
-              double* feats_out) {
-  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
-  std::lock_guard<std::mutex> lk(ctx->mu);
+// The caller holds ctx->mu.
+int glcm_impl_locked(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t owned_rows, size_t pitch,
+                     size_t band_stride, size_t n_bands, int pixel_levels, int levels, const int* distances,
+                     const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out, double* probs_out,
+                     double* feats_out) {
   return guarded([&] {
     check_levels(levels, "glcm");
     check_pixel_levels(pixel_levels, levels);
@@ -924,25 +1027,11 @@ int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size
     }
     auto* d_acc = static_cast<unsigned long long*>(ctx->acc.get(n_out * cells * 8));
     ck(cudaMemsetAsync(d_acc, 0, n_out * cells * 8, s), "memset");
+    if (pixel_levels == levels) clear_sync_flag(ctx, s);
     const bool dev = (flags & TFG_INPUT_DEVICE) != 0;
 
     if (!dev) {
-      // host image(s) -> Scheme-3 stream pipeline over (band, chunk): copy
-      // chunk n+1 while voting chunk n, across band boundaries
-      int dmax = 1;
-      for (int i = 0; i < n_dt; ++i) dmax = std::max(dmax, distances[i]);
-      const size_t k = auto_chunks(width, owned_rows, dmax);
       if (pitch != width) fail(TFG_INVALID_ARGUMENT, "glcm: host images must be dense (pitch == width)");
-      // Pinned caller memory is DMA'd in place. Pageable memory would make
-      // every cudaMemcpyAsync a synchronous bounce-buffer copy, so its rows are
-      // first copied (by several host threads) into the pinned ring slot.
-      const bool pageable = host_memory_kind(px) == 0;
-      if (pageable) {
-        const std::vector<uint64_t> sp = chunk_specs(width, owned_rows, distances, angles_deg, n_dt, k, height);
-        size_t max_rows = 0;
-        for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, sp[3 * i + 2] - sp[3 * i]);
-        for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->hslot[sl].get(max_rows * width + 64);
-      }
       // PCIe is full duplex: a band's counts go down to a pinned counts_out
       // while later bands are still coming up (plain counts, several bands)
       const bool early = n_bands > 1 && counts_out && host_memory_kind(counts_out) == 1 &&
@@ -964,17 +1053,9 @@ int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size
           if (on) cudaStreamSynchronize(st);
         }
       } drain{ctx->aux[0], early};
-      run_pipeline(
-          ctx, width, owned_rows, pixel_levels, levels, distances, angles_deg, n_dt, k, flags, d_acc,
-          [&](size_t b, size_t, size_t start, size_t, size_t buf_end, int sl) -> const uint8_t* {
-            const uint8_t* src = px + b * band_stride + start * width;
-            if (!pageable) return src;
-            uint8_t* dst = static_cast<uint8_t*>(ctx->hslot[sl].p);
-            parallel_memcpy(dst, src, (buf_end - start) * width);
-            return dst;
-          },
-          height, n_bands, band_words, early ? std::function<void(size_t)>(band_done) : nullptr);
-      if (pixel_levels == levels) check_async_flag(ctx, s);
+      host_vote(ctx, px, width, height, owned_rows, band_stride, n_bands, pixel_levels, levels, distances, angles_deg,
+                n_dt, flags, d_acc, early ? std::function<void(size_t)>(band_done) : nullptr);
+      if (pixel_levels == levels) check_sync_flag(ctx, s);
       finish(ctx, d_acc, (int)n_out, levels, flags, counts_out, probs_out, feats_out, s,
              early ? (n_bands - 1) * (size_t)n_dt : 0);
       return;
@@ -996,7 +1077,7 @@ int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size
       d_img = buf;
     }
     if (pixel_levels == levels)
-      launch_validate(ctx, d_img, width, height, dpitch, dstride, (int)n_bands, levels, ctx->d_err, s);
+      launch_validate(ctx, d_img, width, height, dpitch, dstride, (int)n_bands, levels, sync_err(ctx), s);
     for (int t = 0; t < n_dt; ++t) {
       // bands are batched in one launch (blockIdx.y = band); outputs band-major
       // [band][dt][cell]: launch per dt writing with a band stride of n_dt*cells.
@@ -1014,9 +1095,19 @@ int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size
            "scatter");
       }
     }
-    if (pixel_levels == levels) check_async_flag(ctx, s);
+    if (pixel_levels == levels) check_sync_flag(ctx, s);
     finish(ctx, d_acc, (int)n_out, levels, flags, counts_out, probs_out, feats_out, s);
   });
+}
+
+int glcm_impl(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t owned_rows, size_t pitch,
+              size_t band_stride, size_t n_bands, int pixel_levels, int levels, const int* distances,
+              const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out, double* probs_out,
+              double* feats_out) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return glcm_impl_locked(ctx, px, width, height, owned_rows, pitch, band_stride, n_bands, pixel_levels, levels,
+                          distances, angles_deg, n_dt, flags, counts_out, probs_out, feats_out);
 }
 
 }  // namespace
@@ -1060,6 +1151,7 @@ int tfg_glcm_chunked(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels
     const size_t cells = (size_t)levels * levels;
     auto* d_acc = static_cast<unsigned long long*>(ctx->acc.get((size_t)n_dt * cells * 8));
     ck(cudaMemsetAsync(d_acc, 0, (size_t)n_dt * cells * 8, s), "memset");
+    if (pixel_levels == levels) clear_sync_flag(ctx, s);
     const std::vector<uint64_t> specs = chunk_specs(width, height, distances, angles_deg, n_dt, chunk_count);
     size_t max_rows = 0;
     for (size_t i = 0; i < chunk_count; ++i) max_rows = std::max<size_t>(max_rows, specs[3 * i + 2] - specs[3 * i]);
@@ -1082,7 +1174,7 @@ int tfg_glcm_chunked(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels
       cudaStreamSynchronize(ctx->copy);
       throw;
     }
-    if (pixel_levels == levels) check_async_flag(ctx, s);
+    if (pixel_levels == levels) check_sync_flag(ctx, s);
     finish(ctx, d_acc, n_dt, levels, flags, counts_out, probs_out, feats_out, s);
   });
 }
@@ -1114,7 +1206,10 @@ int tfg_subglcms(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, i
     ck(cudaMemcpy2DAsync(d_img, dpitch, px, width, width, height,
                          dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s),
        "stage image");
-    if (pixel_levels == levels) launch_validate(ctx, d_img, width, height, dpitch, 0, 1, levels, ctx->d_err, s);
+    if (pixel_levels == levels) {
+      clear_sync_flag(ctx, s);
+      launch_validate(ctx, d_img, width, height, dpitch, 0, 1, levels, sync_err(ctx), s);
+    }
     // work items: stripe_rows(height, group_count) (parallel.hpp:76-89), cut into <= 64-row pieces
     std::vector<tfg::SubWork> work;
     const size_t base = height / group_count, extra = height % group_count;
@@ -1175,7 +1270,7 @@ int tfg_subglcms(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, i
       ck(cudaMemcpyAsync(counts_out, d_acc, cells * 8, cudaMemcpyDeviceToHost, s), "D2H counts");
     }
     ck(cudaStreamSynchronize(s), "stream sync");
-    if (pixel_levels == levels) check_async_flag(ctx, s);
+    if (pixel_levels == levels) check_sync_flag(ctx, s);
   });
 }
 
@@ -1235,6 +1330,7 @@ int tfg_glcm_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t heigh
                    int pixel_levels, int levels, int distance, int angle_deg, unsigned flags, uint64_t* d_counts,
                    void* stream) {
   if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);  // shared aux streams, events and scratch ordering
   return guarded([&] {
     check_levels(levels, "glcm");
     check_pixel_levels(pixel_levels, levels);
@@ -1256,6 +1352,7 @@ int tfg_glcm_bands_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
                          size_t band_stride, size_t n_bands, int pixel_levels, int levels, int distance,
                          int angle_deg, unsigned flags, uint64_t* d_counts, void* stream) {
   if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);  // shared aux streams, events and scratch ordering
   return guarded([&] {
     check_levels(levels, "glcm");
     check_pixel_levels(pixel_levels, levels);
@@ -1279,6 +1376,7 @@ int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
                          const int* distances, const int* angles_deg, int n_dt, unsigned flags, uint64_t* d_counts,
                          void* stream) {
   if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);  // shared aux streams, events and scratch ordering
   return guarded([&] {
     check_levels(levels, "glcm");
     check_pixel_levels(pixel_levels, levels);
@@ -1327,6 +1425,7 @@ int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
 int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned flags, uint64_t* d_sym_out,
                    double* d_probs_out, double* d_feats_out, void* stream) {
   if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);  // shared aux streams, events and scratch ordering
   return guarded([&] {
     check_levels(levels, "Glcm");
     DeviceGuard dg(ctx->device);
@@ -1355,21 +1454,31 @@ int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned 
 
 int tfg_synth_noise_device(tfg_ctx* ctx, size_t width, size_t height, uint32_t seed, uint8_t* d_out,
                            size_t pitch, void* stream) {
+  if (width < 2 || height < 2) {
+    g_error = "synth_noise: dimensions must be >= 2";
+    return TFG_INVALID_ARGUMENT;
+  }
+  return tfg_synth_noise_rows_device(ctx, width, 0, height, seed, d_out, pitch, stream);
+}
+
+int tfg_synth_noise_rows_device(tfg_ctx* ctx, size_t width, size_t row0, size_t rows, uint32_t seed,
+                                uint8_t* d_out, size_t pitch, void* stream) {
   if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
   std::lock_guard<std::mutex> lk(ctx->mu);
   return guarded([&] {
-    if (width < 2 || height < 2) fail(TFG_INVALID_ARGUMENT, "synth_noise: dimensions must be >= 2");
+    if (width < 2 || rows < 1) fail(TFG_INVALID_ARGUMENT, "synth_noise: dimensions must be >= 2");
     if (!d_out || pitch < width) fail(TFG_INVALID_ARGUMENT, "synth_noise_device: null output or pitch < width");
     DeviceGuard dg(ctx->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const unsigned long long n = (unsigned long long)width * height;
+    const unsigned long long n = (unsigned long long)width * rows;
+    const unsigned long long first = (unsigned long long)width * row0;  // generator output of pixel (row0, 0)
     // up to ~4 segments per SM (each a serial chain of 624-output twists) of
     // >= ~1M outputs: each window costs ~4 ms of host jump-ahead per thread
     const unsigned long long per = (n + (unsigned long long)ctx->num_sms * 4 - 1) / ((unsigned long long)ctx->num_sms * 4);
     const unsigned long long seglen = std::max<unsigned long long>(624ull * 1680, (per + 623) / 624 * 624);
     const size_t nseg = (size_t)((n + seglen - 1) / seglen);
     std::vector<uint32_t> win(nseg * 624);
-    const int rc = tfg_mt19937_windows(seed, 0, seglen, nseg, win.data(), 0);
+    const int rc = tfg_mt19937_windows(seed, first, seglen, nseg, win.data(), 0);
     if (rc != TFG_OK) fail(rc, "synth_noise_device: generator jump-ahead failed");
     uint32_t* d_win = static_cast<uint32_t*>(ctx->mtwin.get(win.size() * sizeof(uint32_t)));
     ck(cudaMemcpyAsync(d_win, win.data(), win.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s), "H2D");
@@ -1383,6 +1492,7 @@ int tfg_synth_noise_device(tfg_ctx* ctx, size_t width, size_t height, uint32_t s
 
 int tfg_check_async_errors(tfg_ctx* ctx) {
   if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
   return guarded([&] {
     DeviceGuard dg(ctx->device);
     ck(cudaDeviceSynchronize(), "sync");
@@ -1396,3 +1506,5 @@ int tfg_check_async_errors(tfg_ctx* ctx) {
 }
 
 }  // extern "C"
+
+#include "tfg_multi_gpu.inc"

@@ -442,7 +442,10 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t 
 // ---------------------------------------------------------------------------
 // Grid-wide barrier for a cooperative (co-resident) launch: every CTA has
 // stored its partial; thread 0 publishes arrival (release) and waits for all
-// `n` CTAs (acquire). The counter is zeroed by the host before the launch.
+// `n` CTAs (acquire). The counter is zero when the launch starts: the host
+// zeroes it once at context creation, and the last CTA to leave each launch
+// re-arms it (glcm_vote_kernel epilogue). Launches that share it never
+// overlap (tfg_engine.cu ScratchOrder).
 // Counter words of a context's cooperative launches: [0] grid barrier,
 // [kExitCtr] CTAs done (re-arm), [32..] shared-pool counters per band.
 constexpr int kExitCtr = 16;

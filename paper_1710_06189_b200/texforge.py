@@ -290,6 +290,23 @@ class Engine:
                                                  C.c_void_p(out.data_ptr()), pitch, C.c_void_p(s)))
         return out
 
+    def synth_noise_rows_device(self, width: int, row0: int, rows: int, seed: int, out=None, pitch: int = 0,
+                                stream=None):
+        """Rows [row0, row0+rows) of synth_noise(width, *, seed) generated on the
+        device (the generator jumps to output row0*width): one GPU's shard of a
+        row-partitioned image. Returns a CUDA uint8 tensor of rows*pitch bytes."""
+        import torch
+        pitch = int(pitch or width)
+        if out is None:
+            out = torch.empty(rows * pitch, dtype=torch.uint8, device=f"cuda:{self.device}")
+        if not out.is_cuda or out.numel() < rows * pitch:
+            raise ValueError("synth_noise_rows_device: out must be a CUDA tensor of >= rows*pitch bytes")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        L.check(self._lib.tfg_synth_noise_rows_device(self.handle, int(width), int(row0), int(rows),
+                                                      seed & 0xFFFFFFFF, C.c_void_p(out.data_ptr()), pitch,
+                                                      C.c_void_p(s)))
+        return out
+
     # -- raw, multi-(d, theta) entry point -------------------------------------
     def glcm(self, pixels: np.ndarray, width: int, height: int, levels: int, dts: Sequence[Tuple[int, int]],
              pixel_levels: int = 256, flags: int = 0, n_bands: int = 1,
