@@ -506,6 +506,14 @@ def run_engine(args, wl):
     plan = Plan(wl, world, rank, tf, D)
     eng = tf.Engine(local)
     lib = Lb.load()
+    # N>1 over NCCL: the library's own communicator (tfg_comm_*: ncclSend/Recv
+    # halo rows, one ncclReduce per step) from a uid rank 0 ships over the
+    # torch.distributed store; gloo test mode keeps torch's collectives.
+    comm = None
+    if dist is not None and backend == "nccl":
+        box = [tf.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        comm = tf.Comm(eng, world, rank, box[0])
     t0 = time.time()
     imgs = make_host_inputs(plan, tf)
     log(f"[rank {rank}] inputs ready in {time.time() - t0:.1f}s")
@@ -519,7 +527,10 @@ def run_engine(args, wl):
         alloc = plan.buffer_rows_alloc() * W if plan.layout != "bands" else px.size
         t = torch.zeros(alloc + 64, dtype=torch.uint8, device="cuda")
         t[: px.size].copy_(torch.from_numpy(px))
-        if plan.layout.startswith("rows") and world > 1:
+        if plan.layout.startswith("rows") and world > 1 and comm is not None:
+            comm.exchange_halo(t.data_ptr(), W, plan.owned, plan.halo, torch.cuda.current_stream().cuda_stream)
+            buf_rows[kind] = plan.owned + (plan.halo if rank + 1 < world else 0)
+        elif plan.layout.startswith("rows") and world > 1:
             buf_rows[kind] = D.exchange_halo(t, plan.owned, W, plan.halo, world, rank)
         else:
             buf_rows[kind] = plan.owned
@@ -593,7 +604,10 @@ def run_engine(args, wl):
         acc.zero_()
         vote_all()
         if dist is not None and plan.layout.startswith("rows"):
-            D.reduce_sum_(acc)  # ONE NCCL reduce of every partial GLCM
+            if comm is not None:  # ONE ncclReduce of every partial GLCM, issued by the library
+                comm.reduce_counts(acc.data_ptr(), acc.numel(), 0, cur["s"].value or 0)
+            else:
+                D.reduce_sum_(acc)
 
     # correctness gate (first step, untimed, rank 0 after the reduce):
     #  * conservation: every GLCM sums to valid_pair_count of the global image;
@@ -771,7 +785,10 @@ def run_engine(args, wl):
             host = out_host
             if dist is not None and plan.layout.startswith("rows"):
                 red.copy_(torch.from_numpy(host.view(np.int64)))
-                D.reduce_sum_(red)
+                if comm is not None:
+                    comm.reduce_counts(red.data_ptr(), red.numel(), 0, torch.cuda.current_stream().cuda_stream)
+                else:
+                    D.reduce_sum_(red)
                 if rank == 0:
                     host = red.cpu().numpy().view(np.uint64)
             return host
@@ -840,6 +857,8 @@ def run_engine(args, wl):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))
+    if comm is not None:
+        comm.close()
     if dist:
         dist.destroy_process_group()
 

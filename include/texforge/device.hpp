@@ -8,6 +8,12 @@
 // state that implies: a process-wide engine context on one CUDA device.
 //
 //   TEXFORGE_DEVICE=<n>   CUDA device of the default context (default 0)
+//   TEXFORGE_GPUS=<n>     n > 1: whole-image GLCMs (compute_glcm_serial and the
+//                         calls built on it) and compute_glcm_chunked run on a
+//                         group of n GPUs with one NCCL communicator
+//                         (tfg_group_*: row shards + d-row halo + one ncclReduce)
+//   TEXFORGE_GPUS_HOST_REDUCE=1  the group may share GPUs and sums through host
+//                         memory (tests of the multi-GPU split on one GPU)
 //
 // Errors: status codes from the C ABI become the reference's exception types
 // with the library's message text (std::invalid_argument for contract
@@ -42,6 +48,31 @@ inline tfg_ctx* context() {
   return ctx;
 }
 
+/// GPUs of the multi-GPU group (TEXFORGE_GPUS, default 1 = no group).
+inline int gpus() {
+  static const int n = [] {
+    const char* env = std::getenv("TEXFORGE_GPUS");
+    const int v = env ? std::atoi(env) : 1;
+    return v > 1 ? v : 1;
+  }();
+  return n;
+}
+
+/// The multi-GPU group (created on first use when gpus() > 1; never destroyed,
+/// like context()).
+inline tfg_group* group() {
+  static tfg_group* g = [] {
+    const char* hr = std::getenv("TEXFORGE_GPUS_HOST_REDUCE");
+    const unsigned flags = (hr && std::atoi(hr) != 0) ? TFG_GROUP_HOST_REDUCE : 0u;
+    tfg_group* out = nullptr;
+    const int rc = tfg_group_create(&out, gpus(), nullptr, flags);
+    if (rc != TFG_OK)
+      throw std::runtime_error(std::string("texforge device: cannot create the GPU group: ") + tfg_last_error());
+    return out;
+  }();
+  return g;
+}
+
 /// Maps a C-ABI status to the reference's exception types.
 inline void check(int rc) {
   if (rc == TFG_OK) return;
@@ -53,6 +84,8 @@ inline void check(int rc) {
 
 /// Number of engine kernels the default context has launched (evidence that
 /// a call ran on the GPU).
-inline std::uint64_t launches() { return tfg_launch_count(context()); }
+inline std::uint64_t launches() {
+  return tfg_launch_count(context()) + (gpus() > 1 ? tfg_group_launch_count(group()) : 0);
+}
 
 }  // namespace texforge::device

@@ -248,8 +248,14 @@ inline Glcm compute_glcm_chunked(ChunkSource& source, const GlcmParams& p, const
   const int d = p.distance, a = to_degrees(p.angle);
   const unsigned flags = mode == ChunkExecution::sequential ? static_cast<unsigned>(TFG_SEQUENTIAL) : 0u;
   Glcm out(p.levels);
-  const int rc = tfg_glcm_chunked(device::context(), width, height, pixel_levels, p.levels, &d, &a, 1, chunk_count,
-                                  &detail::ChunkPump::fetch, &pump, flags, out.counts.data(), nullptr, nullptr);
+  // TEXFORGE_GPUS > 1: the chunks are spread over the GPU group (fetch calls
+  // stay serialised) and the partials meet in one ncclReduce
+  const int rc =
+      device::gpus() > 1
+          ? tfg_group_glcm_chunked(device::group(), width, height, pixel_levels, p.levels, &d, &a, 1, chunk_count,
+                                   &detail::ChunkPump::fetch, &pump, flags, out.counts.data(), nullptr, nullptr)
+          : tfg_glcm_chunked(device::context(), width, height, pixel_levels, p.levels, &d, &a, 1, chunk_count,
+                             &detail::ChunkPump::fetch, &pump, flags, out.counts.data(), nullptr, nullptr);
   if (rc == TFG_SOURCE_ERROR && pump.error) {
     try {
       std::rethrow_exception(pump.error);

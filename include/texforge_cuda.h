@@ -247,7 +247,11 @@ int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned 
  * collective return TFG_COLLECTIVE_ERROR. */
 typedef struct tfg_group tfg_group;
 
-/* devices: n_gpus CUDA ordinals, or NULL for 0..n_gpus-1. */
+/* devices: n_gpus CUDA ordinals, or NULL for 0..n_gpus-1. flags:
+ * TFG_GROUP_HOST_REDUCE sums the partials through host memory instead of
+ * NCCL and lets contexts share a device (testing the multi-GPU split on
+ * fewer GPUs; NCCL refuses two ranks on one GPU). */
+#define TFG_GROUP_HOST_REDUCE (1u << 0)
 int tfg_group_create(tfg_group** out, int n_gpus, const int* devices, unsigned flags);
 void tfg_group_destroy(tfg_group* g);
 int tfg_group_size(const tfg_group* g);

@@ -87,7 +87,27 @@ SIGNATURES = [
     ("tfg_post_async", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p]),
     ("tfg_check_async_errors", C.c_int, [C.c_void_p]),
+    # multi-GPU (tfg_multi_gpu.inc)
+    ("tfg_group_create", C.c_int, [C.POINTER(C.c_void_p), C.c_int, _ip, C.c_uint]),
+    ("tfg_group_destroy", None, [C.c_void_p]),
+    ("tfg_group_size", C.c_int, [C.c_void_p]),
+    ("tfg_group_ctx", C.c_void_p, [C.c_void_p, C.c_int]),
+    ("tfg_group_launch_count", C.c_uint64, [C.c_void_p]),
+    ("tfg_group_glcm", C.c_int, [C.c_void_p, C.c_void_p, _sz, _sz, C.c_int, C.c_int, _ip, _ip, C.c_int, C.c_uint,
+                                 _u64p, _dp, _dp]),
+    ("tfg_group_glcm_bands", C.c_int, [C.c_void_p, C.c_void_p, _sz, _sz, _sz, _sz, C.c_int, C.c_int, _ip, _ip,
+                                       C.c_int, C.c_uint, _u64p, _dp, _dp]),
+    ("tfg_group_glcm_chunked", C.c_int, [C.c_void_p, _sz, _sz, C.c_int, C.c_int, _ip, _ip, C.c_int, _sz, FETCH_FN,
+                                         C.c_void_p, C.c_uint, _u64p, _dp, _dp]),
+    ("tfg_comm_unique_id", C.c_int, [C.c_void_p]),
+    ("tfg_comm_init_rank", C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    ("tfg_comm_destroy", None, [C.c_void_p]),
+    ("tfg_comm_reduce_counts", C.c_int, [C.c_void_p, C.c_void_p, _sz, C.c_int, C.c_void_p]),
+    ("tfg_comm_exchange_halo", C.c_int, [C.c_void_p, C.c_void_p, _sz, _sz, _sz, C.c_void_p]),
+    ("tfg_comm_allreduce_max_f64", C.c_int, [C.c_void_p, C.c_void_p, _sz, C.c_void_p]),
 ]
+TFG_GROUP_HOST_REDUCE = 1
+TFG_COMM_ID_BYTES = 128
 
 _lib = None
 

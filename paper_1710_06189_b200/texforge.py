@@ -374,31 +374,11 @@ class Engine:
         d = (C.c_int * n_dt)(*[int(x[0]) for x in dts])
         a = (C.c_int * n_dt)(*[int(x[1]) for x in dts])
         counts = np.zeros(n_dt * levels * levels, dtype=np.uint64)
-        err_box = {}
-
-        def _fetch(user, idx, start, owned_end, buf_end, dst, err, err_len):
-            try:
-                spec = ChunkSpec(int(idx), int(start), int(owned_end), int(buf_end), int(chunk_count))
-                out = np.ctypeslib.as_array(dst, shape=(int(buf_end - start) * width,))
-                source.fetch(spec, out)
-                return 0
-            except BaseException as e:  # noqa: BLE001 — any source failure aborts the pipeline
-                err_box["exc"] = e
-                msg = str(e).encode()[: max(0, int(err_len) - 1)] + b"\0"
-                if err:
-                    C.memmove(err, msg, len(msg))
-                return 1
-
-        cb = L.FETCH_FN(_fetch)
+        err_box: dict = {}
+        cb = _fetch_callback(source, chunk_count, width, err_box)
         rc = self._lib.tfg_glcm_chunked(self.handle, width, height, pixel_levels, levels, d, a, n_dt,
                                         int(chunk_count), cb, None, flags, _ptr(counts, C.c_uint64), None, None)
-        if rc == L.TFG_SOURCE_ERROR:
-            idx = int(self._lib.tfg_last_error_chunk())
-            exc = err_box.get("exc")
-            if isinstance(exc, PipelineError):
-                raise exc
-            raise PipelineError(idx, self._lib.tfg_last_error().decode(errors="replace"))
-        L.check(rc)
+        _raise_source(self._lib, rc, err_box)
         return counts.reshape(n_dt, levels, levels)
 
     def quantize(self, gray: np.ndarray, levels: int) -> np.ndarray:
@@ -425,6 +405,144 @@ class Engine:
         out = np.empty(5, dtype=np.float64)
         L.check(self._lib.tfg_features(self.handle, _ptr(p, C.c_double), int(levels), _ptr(out, C.c_double)))
         return out
+
+
+def _fetch_callback(source: "ChunkSource", chunk_count: int, width: int, err_box: dict):
+    """A tfg_fetch_fn over ChunkSource.fetch (pipeline.hpp:77-84); the first
+    exception is kept in err_box["exc"] and aborts the pipeline."""
+    def _fetch(user, idx, start, owned_end, buf_end, dst, err, err_len):
+        try:
+            spec = ChunkSpec(int(idx), int(start), int(owned_end), int(buf_end), int(chunk_count))
+            out = np.ctypeslib.as_array(dst, shape=(int(buf_end - start) * width,))
+            source.fetch(spec, out)
+            return 0
+        except BaseException as e:  # noqa: BLE001 — any source failure aborts the pipeline
+            err_box.setdefault("exc", e)
+            msg = str(e).encode()[: max(0, int(err_len) - 1)] + b"\0"
+            if err:
+                C.memmove(err, msg, len(msg))
+            return 1
+    return L.FETCH_FN(_fetch)
+
+
+def _raise_source(lib, rc: int, err_box: dict) -> None:
+    if rc == L.TFG_SOURCE_ERROR:
+        idx = int(lib.tfg_last_error_chunk())
+        exc = err_box.get("exc")
+        if isinstance(exc, PipelineError):
+            raise exc
+        raise PipelineError(idx, lib.tfg_last_error().decode(errors="replace"))
+    L.check(rc)
+
+
+class Group:
+    """Several GPUs of one process behind one NCCL communicator
+    (tfg_group_*): row-partitioned images with a d-row halo
+    and one ncclReduce, band batches sharded with no collective, Scheme 3 with
+    chunks spread over the GPUs. host_reduce=True lets contexts share a GPU
+    (the sum then goes through host memory; NCCL refuses two ranks on one GPU)."""
+
+    def __init__(self, n_gpus: int, devices: Optional[Sequence[int]] = None, host_reduce: bool = False):
+        self._lib = L.load()
+        h = C.c_void_p()
+        devs = (C.c_int * n_gpus)(*devices) if devices is not None else None
+        L.check(self._lib.tfg_group_create(C.byref(h), int(n_gpus), devs,
+                                           L.TFG_GROUP_HOST_REDUCE if host_reduce else 0))
+        self.handle = h
+        self.size = n_gpus
+
+    def close(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            self._lib.tfg_group_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(self._lib.tfg_group_launch_count(self.handle))
+
+    def _dts(self, dts):
+        n = len(dts)
+        return n, (C.c_int * n)(*[int(x[0]) for x in dts]), (C.c_int * n)(*[int(x[1]) for x in dts])
+
+    def glcm(self, pixels: np.ndarray, width: int, height: int, levels: int, dts: Sequence[Tuple[int, int]],
+             pixel_levels: int = 256, flags: int = 0, n_bands: int = 1) -> np.ndarray:
+        """counts[n_bands, n_dt, L, L]: one image row-partitioned over the
+        group (n_bands == 1) or a band batch sharded over it."""
+        px = np.ascontiguousarray(pixels, dtype=np.uint8).reshape(-1)
+        if px.size != width * height * n_bands:
+            raise ValueError("glcm: pixel count does not match dimensions")
+        n_dt, d, a = self._dts(dts)
+        counts = np.zeros(n_bands * n_dt * levels * levels, dtype=np.uint64)
+        if n_bands == 1:
+            rc = self._lib.tfg_group_glcm(self.handle, px.ctypes.data_as(C.c_void_p), width, height, pixel_levels,
+                                          levels, d, a, n_dt, flags, _ptr(counts, C.c_uint64), None, None)
+        else:
+            rc = self._lib.tfg_group_glcm_bands(self.handle, px.ctypes.data_as(C.c_void_p), width, height,
+                                                width * height, n_bands, pixel_levels, levels, d, a, n_dt, flags,
+                                                _ptr(counts, C.c_uint64), None, None)
+        L.check(rc)
+        return counts.reshape(n_bands, n_dt, levels, levels)
+
+    def chunked(self, source: "ChunkSource", dts: Sequence[Tuple[int, int]], chunk_count: int,
+                pixel_levels: int, levels: int, flags: int = 0) -> np.ndarray:
+        width, height = source.width(), source.height()
+        n_dt, d, a = self._dts(dts)
+        counts = np.zeros(n_dt * levels * levels, dtype=np.uint64)
+        err_box: dict = {}
+        cb = _fetch_callback(source, chunk_count, width, err_box)
+        rc = self._lib.tfg_group_glcm_chunked(self.handle, width, height, pixel_levels, levels, d, a, n_dt,
+                                              int(chunk_count), cb, None, flags, _ptr(counts, C.c_uint64), None,
+                                              None)
+        _raise_source(self._lib, rc, err_box)
+        return counts.reshape(n_dt, levels, levels)
+
+
+class Comm:
+    """One rank's NCCL communicator (tfg_comm_*): one process per GPU, the
+    ncclUniqueId shipped by the caller (e.g. torch.distributed)."""
+
+    def __init__(self, engine: Engine, nranks: int, rank: int, uid: bytes):
+        self._lib = L.load()
+        if len(uid) != L.TFG_COMM_ID_BYTES:
+            raise ValueError("Comm: the unique id must be TFG_COMM_ID_BYTES bytes")
+        buf = C.create_string_buffer(uid, L.TFG_COMM_ID_BYTES)
+        h = C.c_void_p()
+        L.check(self._lib.tfg_comm_init_rank(C.byref(h), engine.handle, int(nranks), int(rank), buf))
+        self.handle, self.engine, self.nranks, self.rank = h, engine, nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(L.TFG_COMM_ID_BYTES)
+        L.check(L.load().tfg_comm_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            self._lib.tfg_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reduce_counts(self, d_counts_ptr: int, n: int, root: int = 0, stream: int = 0) -> None:
+        L.check(self._lib.tfg_comm_reduce_counts(self.handle, C.c_void_p(d_counts_ptr), int(n), int(root),
+                                                 C.c_void_p(stream)))
+
+    def exchange_halo(self, d_slab_ptr: int, pitch: int, owned_rows: int, halo: int, stream: int = 0) -> None:
+        L.check(self._lib.tfg_comm_exchange_halo(self.handle, C.c_void_p(d_slab_ptr), int(pitch), int(owned_rows),
+                                                 int(halo), C.c_void_p(stream)))
+
+    def allreduce_max_f64(self, d_ptr: int, n: int, stream: int = 0) -> None:
+        L.check(self._lib.tfg_comm_allreduce_max_f64(self.handle, C.c_void_p(d_ptr), int(n), C.c_void_p(stream)))
 
 
 _engine: Optional[Engine] = None

@@ -27,12 +27,40 @@ def test_header_compiles_standalone(hdr, tmp_path):
     assert r.returncode == 0, r.stderr
 
 
-def _run(binary, timeout=900):
+def _run(binary, timeout=900, env=None):
     path = os.path.join(BUILD, binary)
     if not os.path.exists(path):
         pytest.skip(f"{binary} not built (make -C tests/cpp)")
-    r = subprocess.run([path], capture_output=True, text=True, timeout=timeout)
+    r = subprocess.run([path], capture_output=True, text=True, timeout=timeout,
+                       env=dict(os.environ, **(env or {})))
     return r
+
+
+# TEXFORGE_GPUS=3 on a one-GPU box: three contexts share the GPU and the
+# partials are summed through host memory (NCCL refuses two ranks on one GPU);
+# the row partition, halos and chunk spreading are those of a 3-GPU run.
+GROUP3 = {"TEXFORGE_GPUS": "3", "TEXFORGE_GPUS_HOST_REDUCE": "1"}
+
+
+@pytest.mark.gpu
+def test_multi_gpu_cpp_one_gpu_real_nccl():
+    """tfg_group_create(1): ncclCommInitAll + ncclReduce for real, from C++."""
+    r = _run("multi_gpu_tests")
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+
+
+@pytest.mark.gpu
+def test_multi_gpu_cpp_dropin_group3():
+    r = _run("multi_gpu_tests", env=GROUP3)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+
+
+@pytest.mark.gpu
+def test_reference_unit_suite_on_gpu_group():
+    """The reference's own unit suite with every whole-image and chunked GLCM
+    on the 3-way row-partitioned group path."""
+    r = _run("refsuite_unit", env=GROUP3)
+    assert r.returncode == 0, r.stdout[-6000:] + r.stderr[-6000:]
 
 
 @pytest.mark.gpu
