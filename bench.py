@@ -732,7 +732,13 @@ def run_engine(args, wl):
     bytes_per_call = sum(
         (plan.bands * W * plan.height if plan.layout == "bands" else buf_rows[k] * W) + plan.bands * cells[L] * 8
         for (L, k, _d, _a) in jobs) / len(jobs)
-    achieved = bytes_per_call / (avg_ms / 1e3) / 1e9
+    per_call_achieved = bytes_per_call / (avg_ms / 1e3) / 1e9
+    # the roofline figure comes from the TIMED region: every vote launch of a
+    # step moves bytes_per_call algorithmic bytes; the
+    # step's kernel time is ms_per_step (launch gaps and the accumulator
+    # memset included, so this is the conservative figure). The separate
+    # per-call pass above explains it (per_call).
+    achieved = bytes_per_call * len(jobs) / (ms / 1e3) / 1e9
 
     # end-to-end through the public C ABI from pinned host memory: H2D of this
     # step's inputs inside the region, counts back to the host, NCCL reduce
@@ -824,6 +830,71 @@ def run_engine(args, wl):
                "pinned_h2d_GBps": max(h2d_gbs), "ms_per_step": e2e_s * 1e3,
                "h2d_bound_ms_per_step": h2d / (max(h2d_gbs) * 1e9) * 1e3}
 
+    # Secondary end-to-end line through the C++ drop-in's hottest call, in the
+    # reference CLI's calling convention (R/tools/texforge.cpp:218-236): a
+    # pageable QuantizedImage per input, compute_glcm_privatized(img, p,
+    # plan(L, 49152, nproc)) per (d, theta) -> counts + per_copy_hottest on the
+    # host. The drop-in header forwards it to ONE C-ABI call, tfg_subglcms
+    # (include/texforge/parallel.hpp), which is what is timed here.
+    e2e_dropin = None
+    if not args.no_e2e and world == 1 and plan.layout != "bands":
+        nproc = os.cpu_count() or 1
+        Hd = plan.height
+        qimgs = {}
+        for L in plan.levels_list:
+            pl = tf.plan(L, 49152, nproc)
+            groups = tf._resolve_group_count(0, pl, W, Hd)
+            for kind in plan.kinds:
+                px = imgs[kind][: W * Hd]
+                qimgs[(kind, L)] = (np.array(px) if L == 256 else eng.quantize(px, L), pl, groups)
+        cnt = np.zeros(max(plan.levels_list) ** 2, dtype=np.uint64)
+
+        def dropin_step():
+            for L in plan.levels_list:
+                for kind in plan.kinds:
+                    q, pl, groups = qimgs[(kind, L)]
+                    hot = np.zeros(groups * pl.copies, dtype=np.uint64)
+                    for d, a in plan.dts:
+                        Lb.check(lib.tfg_subglcms(eng.handle, q.ctypes.data_as(C.c_void_p), W, Hd, L, L, d, a,
+                                                  pl.group_size, pl.copies, groups, 0, None,
+                                                  cnt.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                  hot.ctypes.data_as(C.POINTER(C.c_uint64))))
+
+        dropin_step()
+        samples = []
+        for _ in range(max(2, min(args.steps, 5))):
+            t = time.perf_counter()
+            dropin_step()
+            samples.append(time.perf_counter() - t)
+        el = statistics.median(samples)
+
+        # the same calls through compute_glcm_serial's C-ABI call (tfg_glcm, one
+        # (d, theta), same pageable image): the drop-in's reference point
+        def serial_step():
+            for L in plan.levels_list:
+                for kind in plan.kinds:
+                    q, _pl, _g = qimgs[(kind, L)]
+                    for d, a in plan.dts:
+                        dd, aa = C.c_int(d), C.c_int(a)
+                        Lb.check(lib.tfg_glcm(eng.handle, q.ctypes.data_as(C.c_void_p), W, Hd, W, L, L,
+                                              C.byref(dd), C.byref(aa), 1, 0,
+                                              cnt.ctypes.data_as(C.POINTER(C.c_uint64)), None, None))
+
+        serial_step()
+        ss = []
+        for _ in range(max(2, min(args.steps, 5))):
+            t = time.perf_counter()
+            serial_step()
+            ss.append(time.perf_counter() - t)
+        el_serial = statistics.median(ss)
+        e2e_dropin = {"value": pairs_per_step / el / 1e9, "unit": UNIT, "ms_per_step": el * 1e3,
+                      "serial_value": pairs_per_step / el_serial / 1e9, "serial_ms_per_step": el_serial * 1e3,
+                      "privatized_over_serial_time": el / el_serial,
+                      "h2d_bytes_per_step": len(jobs) * W * Hd,
+                      "d2h_bytes_per_step": sum(L * L * 8 for (L, _k, _d, _a) in jobs),
+                      "api": "texforge::compute_glcm_privatized (C++ drop-in) = tfg_subglcms on a pageable image, "
+                             "plan(L, 49152, nproc), one call per (input, d, theta) as in the reference CLI bench"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -850,8 +921,14 @@ def run_engine(args, wl):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": committed_traffic(wl),
                          "kernel": "glcm_vote_kernel (+ its split-K partial reduce for L*L > 4096): one engine call",
-                         "bytes_per_launch": bytes_per_call, "avg_launch_ms": avg_ms, "peak_source": peak_src},
+                         "bytes_per_launch": bytes_per_call, "launches_per_step": len(jobs),
+                         "basis": "bytes_per_launch x launches_per_step / ms_per_step (timed region, per GPU)",
+                         "per_call": {"avg_launch_ms": avg_ms, "achieved": per_call_achieved,
+                                      "frac": per_call_achieved / peak,
+                                      "how": "separate pass, CUDA events around each engine call on its stream"},
+                         "peak_source": peak_src},
             "e2e": e2e,
+            "e2e_dropin": e2e_dropin,
             "gpu_launches": gpu_launches,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

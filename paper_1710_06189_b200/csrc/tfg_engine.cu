@@ -70,6 +70,10 @@ struct DevBuf {
     p = nullptr;
     cap = 0;
     ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    // zeroed once at allocation: the row padding and tail slack of the image
+    // buffers are read (never voted) by the 16-byte segment loads, so they
+    // must hold defined bytes (compute-sanitizer initcheck)
+    ck(cudaMemset(p, 0, bytes), "memset");
     cap = bytes;
     return p;
   }
@@ -779,6 +783,34 @@ void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, i
                      acc_band_stride, band_done);
 }
 
+// Shared-memory budget of glcm_subglcm_kernel's R sub-GLCM copies.
+constexpr size_t kSubSmemBytes = 96 * 1024;
+
+// Host raster -> a pitched device buffer at PCIe speed: pinned caller memory
+// goes by DMA; pageable rows are first copied by several host threads into
+// the pinned ring slots, each slot's H2D overlapping the next slot's fill.
+void stage_host_image(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, uint8_t* d_dst,
+                      size_t dpitch) {
+  cudaStream_t s = ctx->exec;
+  if (host_memory_kind(px) != 0) {
+    ck(cudaMemcpy2DAsync(d_dst, dpitch, px, width, width, height, cudaMemcpyHostToDevice, s), "stage image");
+    return;
+  }
+  const size_t rows_per = std::max<size_t>(1, (size_t)(16u << 20) / std::max<size_t>(width, 1));
+  for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->hslot[sl].get(rows_per * width + 64);
+  size_t n = 0;
+  for (size_t r = 0; r < height; r += rows_per, ++n) {
+    const int sl = (int)(n % tfg_ctx::kSlots);
+    const size_t rows = std::min(rows_per, height - r);
+    if (n >= (size_t)tfg_ctx::kSlots) ck(cudaEventSynchronize(ctx->copied[sl]), "event sync");
+    uint8_t* slot = static_cast<uint8_t*>(ctx->hslot[sl].p);
+    parallel_memcpy(slot, px + r * width, rows * width);
+    ck(cudaMemcpy2DAsync(d_dst + r * dpitch, dpitch, slot, width, width, rows, cudaMemcpyHostToDevice, s),
+       "stage image");
+    ck(cudaEventRecord(ctx->copied[sl], s), "event record");
+  }
+}
+
 // Host image(s) -> the Scheme-3 stream pipeline over (band, chunk), votes
 // added into d_acc ([band][dt][cell]): copy chunk n+1 while voting chunk n,
 // across band boundaries. `height` buffer rows of which anchors in rows
@@ -1203,12 +1235,69 @@ int tfg_subglcms(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, i
     const size_t dpitch = round16(width);
     uint8_t* d_img = static_cast<uint8_t*>(ctx->img.get(dpitch * height + 64));
     const bool dev = (flags & TFG_INPUT_DEVICE) != 0;
-    ck(cudaMemcpy2DAsync(d_img, dpitch, px, width, width, height,
-                         dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s),
-       "stage image");
+    if (dev) {
+      ck(cudaMemcpy2DAsync(d_img, dpitch, px, width, width, height, cudaMemcpyDeviceToDevice, s), "stage image");
+    } else {
+      stage_host_image(ctx, px, width, height, d_img, dpitch);
+    }
     if (pixel_levels == levels) {
       clear_sync_flag(ctx, s);
       launch_validate(ctx, d_img, width, height, dpitch, 0, 1, levels, sync_err(ctx), s);
+    }
+    long sdr, sdc;
+    offset_of(distance, angle_deg, &sdr, &sdc);
+    if (copies == 1 && cells * 4 > kSubSmemBytes && group_count <= 4 * (size_t)ctx->num_sms &&
+        height / group_count >= (size_t)sdr) {
+      // One copy per group and a sub-GLCM too large for shared memory: sub-GLCM
+      // g is the GLCM of stripe g's anchors (lane routing is moot with one
+      // copy), so the stripes vote through the privatised kernel as bands of
+      // one launch (band b = stripe b's rows + the halo rows below it, read in
+      // place), instead of per-pixel global atomics.
+      std::vector<size_t> row0(group_count + 1);
+      const size_t base = height / group_count, extra = height % group_count;
+      for (size_t g = 0; g < group_count; ++g) row0[g + 1] = row0[g] + base + (g < extra ? 1 : 0);
+      auto* d_st = static_cast<unsigned long long*>(ctx->acc.get((group_count + 1) * cells * 8 + n_subs * 8));
+      auto* d_cnt = d_st + group_count * cells;
+      auto* d_max = d_cnt + cells;
+      ck(cudaMemsetAsync(d_st, 0, group_count * cells * 8, s), "memset");
+      const long dr = sdr;  // stripes are >= dr rows: every halo lies in the next stripe
+      const unsigned vflags = flags & ~TFG_INPUT_DEVICE;
+      // bands of equal geometry: [0, extra) (base+1 rows), [extra, G-1) and the
+      // last stripe (base rows; the last one has no rows below it)
+      auto run = [&](size_t g0, size_t g1) {
+        if (g0 >= g1) return;
+        const size_t rows = row0[g0 + 1] - row0[g0];
+        const size_t below = height - row0[g1 - 1] - rows;  // rows after the group's last stripe
+        const size_t halo = std::min<size_t>((size_t)std::max<long>(dr, 0), below);
+        launch_vote(ctx, d_img + row0[g0] * dpitch, width, rows + halo, dpitch, rows * dpitch, (int)(g1 - g0), rows,
+                    pixel_levels, levels, distance, angle_deg, vflags, d_st + g0 * cells, s);
+      };
+      const size_t split = std::min(extra, group_count - 1);
+      run(0, split);
+      run(split, group_count - 1);
+      run(group_count - 1, group_count);
+      tfg::stripe_sum_kernel<<<(unsigned)std::min<size_t>((cells + 255) / 256, 1024), 256, 0, s>>>(
+          d_st, (int)cells, (int)group_count, counts_out ? d_cnt : nullptr, nullptr);
+      ck(cudaGetLastError(), "stripe_sum_kernel launch");
+      ctx->launches++;
+      if (per_copy_hottest_out) {
+        tfg::stripe_max_kernel<<<(unsigned)group_count, 256, 0, s>>>(d_st, (int)cells, d_max);
+        ck(cudaGetLastError(), "stripe_max_kernel launch");
+        ctx->launches++;
+        ck(cudaMemcpyAsync(per_copy_hottest_out, d_max, n_subs * 8, cudaMemcpyDeviceToHost, s), "D2H max");
+      }
+      if (subs_out) {
+        uint32_t* d_subs = static_cast<uint32_t*>(ctx->tmp.get(n_subs * cells * 4));
+        tfg::stripe_sum_kernel<<<(unsigned)std::min<size_t>((cells + 255) / 256, 1024), 256, 0, s>>>(
+            d_st, (int)cells, (int)group_count, nullptr, d_subs);
+        ck(cudaGetLastError(), "stripe_sum_kernel launch");
+        ctx->launches++;
+        ck(cudaMemcpyAsync(subs_out, d_subs, n_subs * cells * 4, cudaMemcpyDeviceToHost, s), "D2H subs");
+      }
+      if (counts_out) ck(cudaMemcpyAsync(counts_out, d_cnt, cells * 8, cudaMemcpyDeviceToHost, s), "D2H counts");
+      ck(cudaStreamSynchronize(s), "stream sync");
+      if (pixel_levels == levels) check_sync_flag(ctx, s);
+      return;
     }
     // work items: stripe_rows(height, group_count) (parallel.hpp:76-89), cut into <= 64-row pieces
     std::vector<tfg::SubWork> work;
@@ -1247,7 +1336,7 @@ int tfg_subglcms(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, i
     sp.work = d_work;
     sp.subs = d_subs;
     const size_t smem = copies * cells * 4;
-    sp.use_smem = smem <= 96 * 1024;
+    sp.use_smem = smem <= kSubSmemBytes;
     if (sp.use_smem && smem > 48 * 1024)
       ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(tfg::glcm_subglcm_kernel),
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),

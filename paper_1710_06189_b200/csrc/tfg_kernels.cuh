@@ -1003,6 +1003,41 @@ __global__ void __launch_bounds__(256) subglcm_max_kernel(const uint32_t* __rest
   }
 }
 
+// One copy per group (plan.copies == 1, the reference's plan for L >= 128 at
+// its default scratch budget): sub-GLCM g is the GLCM of stripe g's anchors,
+// voted by glcm_vote_kernel with the stripes as bands. These two kernels turn
+// the [groups][cells] u64 stripe GLCMs into the reduce_subglcms sum
+// (parallel.hpp:228-237) and the per_copy_hottest maxima (:247-252), and the
+// u32 sub-GLCM export (u32 by the reference's 2^32 votes-per-group floor).
+__global__ void __launch_bounds__(256) stripe_max_kernel(const unsigned long long* __restrict__ stripes, int cells,
+                                                         unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long s[8];
+  const unsigned long long* g = stripes + (size_t)blockIdx.x * cells;
+  unsigned long long m = 0;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) m = max(m, g[c]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = max(m, s[i]);
+    out[blockIdx.x] = m;
+  }
+}
+
+__global__ void stripe_sum_kernel(const unsigned long long* __restrict__ stripes, int cells, int groups,
+                                  unsigned long long* __restrict__ counts, uint32_t* __restrict__ subs32) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) {
+    unsigned long long t = 0;
+    for (int g = 0; g < groups; ++g) {
+      const unsigned long long v = stripes[(size_t)g * cells + c];
+      t += v;
+      if (subs32) subs32[(size_t)g * cells + c] = (uint32_t)v;
+    }
+    if (counts) counts[c] = t;
+  }
+}
+
 // Validation of an already-quantised raster (QuantizedImage ctor, image.hpp:46-48).
 __global__ void validate_levels_kernel(const uint8_t* img, unsigned long long pitch, int width,
                                        long long rows, unsigned long long band_stride, int levels,

@@ -376,6 +376,29 @@ def test_python_subglcms_and_per_copy_hottest(copies, groups):
     assert st.per_copy_hottest == [int(x) for x in want.max(axis=1)]
 
 
+@pytest.mark.parametrize("L,groups,d,a,kind", [(256, 1, 1, 0, "noise"), (256, 7, 2, 45, "smooth"),
+                                                (181, 32, 3, 135, "noise"), (256, 40, 1, 90, "smooth"),
+                                                (200, 5, 4, 90, "noise")])
+def test_privatized_one_copy_stripe_path(L, groups, d, a, kind):
+    # plan.copies == 1 with sub-GLCMs over the shared-memory budget (the
+    # reference's own plan at L >= 157): stripes voted as bands of one launch,
+    # sum + per-stripe maxima on the device; exact vs the numpy restatement
+    w, h = 333, 211
+    gray = (tf.synth_noise if kind == "noise" else tf.synth_smooth)(w, h, 9).pixels
+    q = O.quantize(gray, L)
+    img = tf.QuantizedImage(w, h, L, q)
+    p = tf.GlcmParams(d, tf.angle_from_degrees(a), L)
+    plan = tf.plan(L, tf.kDefaultScratchBudget, 4)
+    assert plan.copies == 1
+    want = _subglcms_numpy(q, w, h, L, d, a, plan.group_size, 1, groups)
+    g, st = tf.compute_glcm_privatized(img, p, plan, groups)
+    assert np.array_equal(g.counts, want.sum(axis=0).astype(np.uint64))
+    assert st.per_copy_hottest == [int(x) for x in want.max(axis=1)]
+    subs = tf.compute_subglcms(img, p, plan, groups)
+    for i in range(groups):
+        assert np.array_equal(subs[i], want[i]), i
+
+
 @pytest.mark.parametrize("levels", [16, 64, 256])
 def test_multi_async_all_dts_bands_row_end(engine, levels):
     # tfg_glcm_multi_async: every (d, theta) in one call; L <= 64 forks the

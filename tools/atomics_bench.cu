@@ -22,11 +22,29 @@ enum Mode {
   M_RANDOM_8WAY,            // COPIES8 layout: random cell*8 + lane%8 over 16K words
   M_RANDOM_8WAY_RET,        // same, returning (what a drain check would need)
   M_PACKED_16WAY_RET,       // L=64 candidate: 16 copies of packed u16 pairs, word*16 + lane%16, returning
+  // The modes above draw addresses from a per-thread LCG whose 32 lanes form an
+  // arithmetic progression: banks are quasi-random (2.48 wavefronts per warp
+  // ATOMS instead of 3.53 for independent cells). The hashed modes below pass
+  // the LCG state through murmur3's finaliser so every lane's word is
+  // independent, like a noise image's GLCM cells.
+  M_HASH_128KB_INC,         // random word in 128 KB, hashed (L=256 PACKED16 on noise)
+  M_HASH_128KB_RET,         // same, returning (the PACKED16 drain check)
+  M_HASH_8WAY_INC,          // COPIES8 layout, hashed cells (L=64 on noise)
+  M_HASH_16WAY_RET,         // 16 copies of packed u16 pairs, hashed cells, returning
   M_NMODES
 };
 const char* kNames[] = {"lane_private_inc", "lane_private_addn", "random_128KB_inc", "random_128KB_ret",
                         "random_16KB_inc", "same_addr_inc", "same_addr_addn", "lds_sts_private",
-                        "copies8_random", "copies8_random_ret", "packed16x16_random_ret"};
+                        "copies8_random", "copies8_random_ret", "packed16x16_random_ret",
+                        "hashed_128KB_inc", "hashed_128KB_ret", "hashed_copies8_inc", "hashed_packed16x16_ret"};
+
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  return h ^ (h >> 16);
+}
 
 template <int mode>
 __global__ void __launch_bounds__(kT, 1) bench(unsigned long long* cycles, uint32_t* sink) {
@@ -60,6 +78,18 @@ __global__ void __launch_bounds__(kT, 1) bench(unsigned long long* cycles, uint3
       case M_PACKED_16WAY_RET:
         acc |= atomicAdd(&s[((r & 2047) << 4) | (lane & 15)], 1u << ((h >> 3) & 16));
         break;
+      case M_HASH_128KB_INC: atomicAdd(&s[fmix32(h) & 32767], 1u); break;
+      case M_HASH_128KB_RET: {
+        const uint32_t x = fmix32(h);
+        acc |= atomicAdd(&s[x & 32767], 1u << ((x >> 15) & 16));
+        break;
+      }
+      case M_HASH_8WAY_INC: atomicAdd(&s[((fmix32(h) & 4095) << 3) | (lane & 7)], 1u); break;
+      case M_HASH_16WAY_RET: {
+        const uint32_t x = fmix32(h);
+        acc |= atomicAdd(&s[((x & 2047) << 4) | (lane & 15)], 1u << ((x >> 11) & 16));
+        break;
+      }
     }
   }
   const unsigned long long t1 = clock64();
@@ -122,8 +152,8 @@ int main() {
   cudaMalloc(&cyc, 8);
   cudaMalloc(&sink, 64);
   using K = void (*)(unsigned long long*, uint32_t*);
-  K ks[M_NMODES] = {bench<0>, bench<1>, bench<2>, bench<3>, bench<4>, bench<5>,
-                    bench<6>, bench<7>, bench<8>, bench<9>, bench<10>};
+  K ks[M_NMODES] = {bench<0>, bench<1>, bench<2>, bench<3>, bench<4>, bench<5>, bench<6>, bench<7>,
+                    bench<8>, bench<9>, bench<10>, bench<11>, bench<12>, bench<13>, bench<14>};
   for (auto k : ks) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
