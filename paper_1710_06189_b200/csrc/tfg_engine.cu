@@ -74,6 +74,9 @@ struct DevBuf {
     // buffers are read (never voted) by the 16-byte segment loads, so they
     // must hold defined bytes (compute-sanitizer initcheck)
     ck(cudaMemset(p, 0, bytes), "memset");
+    // the memset runs on the legacy stream, which does not order against the
+    // context's non-blocking streams: finish it before the buffer is handed out
+    ck(cudaStreamSynchronize(nullptr), "memset sync");
     cap = bytes;
     return p;
   }
