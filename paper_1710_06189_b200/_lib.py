@@ -112,6 +112,24 @@ TFG_COMM_ID_BYTES = 128
 _lib = None
 
 
+def _prefer_torch_nccl() -> None:
+    """The library dlopens NCCL on its first multi-GPU call (csrc/tfg_nccl_dl.h).
+    In a Python process that NCCL must be torch's bundled copy: one process
+    keeps the first libnccl.so.2 it maps, and libtorch_cuda needs its own."""
+    if os.environ.get("TEXFORGE_NCCL_LIB"):
+        return
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        spec = None
+    for d in (spec.submodule_search_locations if spec else None) or []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            os.environ["TEXFORGE_NCCL_LIB"] = p
+            return
+
+
 def load() -> C.CDLL:
     """Loads the in-tree engine library; raises if it was not built."""
     global _lib
@@ -120,6 +138,7 @@ def load() -> C.CDLL:
             raise RuntimeError(
                 f"libtexforge_cuda.so not found at {LIB_PATH}: run __graft_entry__.build() "
                 "(there is no CPU fallback)")
+        _prefer_torch_nccl()
         lib = C.CDLL(LIB_PATH)
         for name, res, args in SIGNATURES:
             fn = getattr(lib, name)

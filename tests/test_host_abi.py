@@ -6,6 +6,7 @@ import ctypes as C
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -39,6 +40,21 @@ def test_header_symbols_exported():
 def test_library_is_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", L.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_no_link_time_nccl_and_torch_imports_after_the_library():
+    """NCCL is dlopened on the first multi-GPU call (csrc/tfg_nccl_dl.h). A
+    link-time libnccl.so.2 (the system 2.27) would be the copy a later
+    `import torch` binds to, and libtorch_cuda fails on a 2.28-only symbol —
+    the order smoke() and the drop-in take (library first, torch second)."""
+    needed = subprocess.run(["readelf", "-d", L.LIB_PATH], capture_output=True, text=True).stdout
+    assert "libnccl" not in needed
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_1710_06189_b200 import _lib; _lib.load()\n"
+            "import torch; print('ok', torch.__version__)\n") % ROOT
+    env = {k: v for k, v in os.environ.items() if k != "TEXFORGE_NCCL_LIB"}
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stderr[-2000:]
 
 
 def test_abi_version():
