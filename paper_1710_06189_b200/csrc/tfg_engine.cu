@@ -217,35 +217,20 @@ size_t hist_words_of(int strat, int levels) {
 
 using VoteKernel = void (*)(const tfg::VoteParams);
 
-template <int Q, int S>
-VoteKernel pick_k(int ksel) {
-  switch (ksel) {
-    case 0: return tfg::glcm_vote_kernel<Q, S, 0>;
-    case 1: return tfg::glcm_vote_kernel<Q, S, 1>;
-    case 2: return tfg::glcm_vote_kernel<Q, S, 2>;
-    case 3: return tfg::glcm_vote_kernel<Q, S, 3>;
-    case 5: return tfg::glcm_vote_kernel<Q, S, 5>;
-    case 6: return tfg::glcm_vote_kernel<Q, S, 6>;
-    case 7: return tfg::glcm_vote_kernel<Q, S, 7>;
-    case 8: return tfg::glcm_vote_kernel<Q, S, 8>;
-    default: return tfg::glcm_vote_kernel<Q, S, 4>;
-  }
-}
-template <int Q>
-VoteKernel pick_s(int strat, int ksel) {
-  switch (strat) {
-    case tfg::S_COPIES32: return pick_k<Q, tfg::S_COPIES32>(ksel);
-    case tfg::S_COPIES8: return pick_k<Q, tfg::S_COPIES8>(ksel);
-    case tfg::S_COPY1: return pick_k<Q, tfg::S_COPY1>(ksel);
-    default: return pick_k<Q, tfg::S_PACKED16>(ksel);
-  }
-}
+// The glcm_vote_kernel instantiations live in tfg_vote_q{0..3}.cu (one
+// translation unit per quantiser, compiled in parallel): tfg_vote_inst.cu.
+}  // namespace
+VoteKernel tfg_pick_vote_q0(int strat, int ksel);
+VoteKernel tfg_pick_vote_q1(int strat, int ksel);
+VoteKernel tfg_pick_vote_q2(int strat, int ksel);
+VoteKernel tfg_pick_vote_q3(int strat, int ksel);
+namespace {
 VoteKernel pick_vote(int quant, int strat, int ksel) {
   switch (quant) {
-    case tfg::Q_NONE: return pick_s<tfg::Q_NONE>(strat, ksel);
-    case tfg::Q_CLAMP: return pick_s<tfg::Q_CLAMP>(strat, ksel);
-    case tfg::Q_SHIFT: return pick_s<tfg::Q_SHIFT>(strat, ksel);
-    default: return pick_s<tfg::Q_MUL>(strat, ksel);
+    case tfg::Q_NONE: return tfg_pick_vote_q0(strat, ksel);
+    case tfg::Q_CLAMP: return tfg_pick_vote_q1(strat, ksel);
+    case tfg::Q_SHIFT: return tfg_pick_vote_q2(strat, ksel);
+    default: return tfg_pick_vote_q3(strat, ksel);
   }
 }
 template <int Q>

@@ -214,7 +214,7 @@ __device__ __forceinline__ void packed_drain(uint32_t addr, uint32_t x, unsigned
 
 // Rare path, out of line so the hot loop fits the instruction cache: drain
 // the words of the pixels in `mask` of one item.
-__device__ __noinline__ void packed_drain_item(uint32_t hb, uint32_t P0, uint32_t P1, uint32_t P2, uint32_t P3,
+static __device__ __noinline__ void packed_drain_item(uint32_t hb, uint32_t P0, uint32_t P1, uint32_t P2, uint32_t P3,
                                                uint32_t Q0, uint32_t Q1, uint32_t Q2, uint32_t Q3, uint32_t mask,
                                                unsigned long long* glcm, uint32_t L) {
   const uint32_t P[4] = {P0, P1, P2, P3}, Q[4] = {Q0, Q1, Q2, Q3};
@@ -845,6 +845,9 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   }
 }
 
+// Everything below is used by tfg_engine.cu only (tfg_vote_inst.cu defines
+// TFG_VOTE_ONLY: its translation units hold just the vote kernels).
+#ifndef TFG_VOTE_ONLY
 // Sum of per-CTA PACKED16 words into the u64 accumulator. Split-K: CTA
 // (x, y) sums partials [y*per, (y+1)*per) of words [4*(x*256+t), +4) with
 // 16-byte loads, then adds its 8 cell sums with u64 atomics (spread addresses).
@@ -1256,5 +1259,7 @@ __global__ void __launch_bounds__(256) synth_noise_kernel(const uint32_t* __rest
     __syncthreads();  // the next twist overwrites mt
   }
 }
+
+#endif  // TFG_VOTE_ONLY
 
 }  // namespace tfg

@@ -1,0 +1,41 @@
+// tfg_vote_inst.cu — the glcm_vote_kernel instantiations of one quantiser
+// (TFG_QUANT = tfg::Quant), compiled once per quantiser as tfg_vote_q<N>.o so
+// the four sets build in parallel. tfg_engine.cu dispatches through
+// tfg_pick_vote_q<N>(strat, ksel).
+#define TFG_VOTE_ONLY
+#include "tfg_kernels.cuh"
+
+#ifndef TFG_QUANT
+#error "define TFG_QUANT (0..3)"
+#endif
+
+using VoteKernel = void (*)(const tfg::VoteParams);
+
+namespace {
+template <int Q, int S>
+VoteKernel pick_k(int ksel) {
+  switch (ksel) {
+    case 0: return tfg::glcm_vote_kernel<Q, S, 0>;
+    case 1: return tfg::glcm_vote_kernel<Q, S, 1>;
+    case 2: return tfg::glcm_vote_kernel<Q, S, 2>;
+    case 3: return tfg::glcm_vote_kernel<Q, S, 3>;
+    case 5: return tfg::glcm_vote_kernel<Q, S, 5>;
+    case 6: return tfg::glcm_vote_kernel<Q, S, 6>;
+    case 7: return tfg::glcm_vote_kernel<Q, S, 7>;
+    case 8: return tfg::glcm_vote_kernel<Q, S, 8>;
+    default: return tfg::glcm_vote_kernel<Q, S, 4>;
+  }
+}
+}  // namespace
+
+#define TFG_CAT2(a, b) a##b
+#define TFG_CAT(a, b) TFG_CAT2(a, b)
+VoteKernel TFG_CAT(tfg_pick_vote_q, TFG_QUANT)(int strat, int ksel) {
+  constexpr int Q = TFG_QUANT;
+  switch (strat) {
+    case tfg::S_COPIES32: return pick_k<Q, tfg::S_COPIES32>(ksel);
+    case tfg::S_COPIES8: return pick_k<Q, tfg::S_COPIES8>(ksel);
+    case tfg::S_COPY1: return pick_k<Q, tfg::S_COPY1>(ksel);
+    default: return pick_k<Q, tfg::S_PACKED16>(ksel);
+  }
+}
