@@ -271,6 +271,16 @@ long long pool_pct() {
   return v;
 }
 
+// Line-aligned interior segments (make_geometry); TEXFORGE_ALIGN=0 turns
+// them off for A/B timing.
+bool align_interior_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("TEXFORGE_ALIGN");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // Every vote kernel gets the full 227 KB dynamic shared-memory opt-in once;
 // occupancy is then queried per (kernel, smem) pair.
 std::mutex g_kinfo_mu;
@@ -330,7 +340,7 @@ struct VoteGeometry {
 };
 
 VoteGeometry make_geometry(size_t width, size_t height, size_t pitch, size_t row_end, int levels,
-                           int pixel_levels, int distance, int angle) {
+                           int pixel_levels, int distance, int angle, bool align_interior = false) {
   VoteGeometry g;
   long dr, dc;
   offset_of(distance, angle, &dr, &dc);
@@ -363,9 +373,24 @@ VoteGeometry make_geometry(size_t width, size_t height, size_t pitch, size_t row
   // row run unmasked in the main pass; rows too narrow for 64-segment double
   // batches go entirely through the edge pass
   if (p.nch >= 66) {
+    p.js = 1;
     p.ni = p.nch - 2;
-    p.ne = 2;
+    if (align_interior && pitch % 128 == 0) {
+      // interior segments start on a 128-byte line (the rows do, when the
+      // buffer is 128-byte aligned: launch_vote checks the pointer), and
+      // ni % 8 == 0 keeps every double batch (64 segments) line-aligned, so
+      // a warp's 512-byte LDG.128 touches 4 lines instead of 5. The up to
+      // 14 extra edge segments per row go through the masked edge pass.
+      const int js = 1 + ((8 - ((p.ch0 + 1) & 7)) & 7);
+      const int ni = (p.nch - 1 - js) / 8 * 8;
+      if (ni >= 64) {
+        p.js = js;
+        p.ni = ni;
+      }
+    }
+    p.ne = p.nch - p.ni;
   } else {
+    p.js = 1;
     p.ni = 0;
     p.ne = std::max(p.nch, 1);
   }
@@ -435,7 +460,9 @@ struct ScratchOrder {
 void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
                  size_t band_stride, int n_bands, size_t row_end, int pixel_levels, int levels,
                  int distance, int angle, unsigned flags, unsigned long long* d_glcm, cudaStream_t s) {
-  VoteGeometry g = make_geometry(width, height, pitch, row_end, levels, pixel_levels, distance, angle);
+  const bool aligned = align_interior_enabled() && reinterpret_cast<uintptr_t>(d_img) % 128 == 0 &&
+                       (n_bands == 1 || band_stride % 128 == 0);
+  VoteGeometry g = make_geometry(width, height, pitch, row_end, levels, pixel_levels, distance, angle, aligned);
   if (g.empty) return;
   tfg::VoteParams& p = g.p;
   p.img = d_img;

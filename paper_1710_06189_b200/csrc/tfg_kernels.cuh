@@ -32,7 +32,10 @@
 
 namespace tfg {
 
-constexpr int kThreads = 1024;  // threads per vote CTA (32 warps)
+#ifndef TFG_THREADS
+#define TFG_THREADS 1024
+#endif
+constexpr int kThreads = TFG_THREADS;  // threads per vote CTA (32 warps)
 
 enum Quant : int {
   Q_NONE = 0,   // values used as-is (gray with L=256, or quantised with L=256)
@@ -83,6 +86,7 @@ struct VoteParams {
   // two-pass decomposition (glcm_vote_kernel): interior segments j in [1, nch-1)
   // of every anchor row (main pass, no masks) and the rest (edge pass)
   int ni;                           // interior segments per row (0: everything is edge work)
+  int js;                           // first interior segment (>= 1; 128-B aligned when the rows are)
   uint32_t ni_mul, ni_shr;          // fast division by ni
   long long main_items;             // nrows * ni
   long long main_per_cta;           // multiple of 64; CTA ranges tile [0, pool_beg)
@@ -254,6 +258,21 @@ __device__ __noinline__ void vote_masked(uint32_t hb, uint32_t P0, uint32_t P1, 
   }
 }
 
+// The 16 PACKED16 votes of an unmasked item (returning atomics, then the
+// drain rule of kDrainBit). Reference bytes with the half bit cleared: PRMT
+// then yields the word index a + 256 (b & 127) directly (no per-vote mask).
+__device__ __forceinline__ void packed_vote16(uint32_t hb, const uint32_t (&P)[4], const uint32_t (&Q)[4],
+                                              unsigned long long* glcm, uint32_t L) {
+  uint32_t flag = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t Qm = Q[i] & 0x7F7F7F7Fu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) flag |= atom_smem(hb + pair_x(P[i], Qm, j) * 4u, packed_inc(Q[i], j));
+  }
+  if (flag & kDrainBit) packed_drain_item(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], 0xFFFFu, glcm, L);
+}
+
 // Votes the 16 pixel pairs of one item. Returns true when the run-length
 // shortcut fired (all 16 pairs identical: one vote of weight 16).
 template <int STRAT>
@@ -274,17 +293,7 @@ __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], cons
       }
     }
     if constexpr (STRAT == S_PACKED16) {
-      // reference bytes with the half bit cleared: PRMT then yields the word
-      // index a + 256 (b & 127) directly (no per-vote mask)
-      uint32_t flag = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t Qm = Q[i] & 0x7F7F7F7Fu;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) flag |= atom_smem(hb + pair_x(P[i], Qm, j) * 4u, packed_inc(Q[i], j));
-      }
-      if (flag & kDrainBit)
-        packed_drain_item(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], 0xFFFFu, glcm, L);
+      packed_vote16(hb, P, Q, glcm, L);
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -306,8 +315,21 @@ __device__ __forceinline__ uint32_t cell_pos(uint32_t b, uint32_t a) {
   else return a + 256u * b;
 }
 
+#ifndef TFG_LDG_MODE
+#define TFG_LDG_MODE 0
+#endif
 __device__ __forceinline__ uint4 ldg16(const uint8_t* p) {
+#if TFG_LDG_MODE == 1
+  uint4 v;  // L2 only (no L1 allocation)
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+#elif TFG_LDG_MODE == 2
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+#else
   return __ldg(reinterpret_cast<const uint4*>(p));
+#endif
 }
 
 // Bulk prefetch of [a, a+bytes) into L2 (cp.async.bulk.prefetch.L2, sm_90+):
@@ -616,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   const uint32_t lane16 = lane << 4;
   // 64-bit bases are formed once; per double batch one row offset, per item
   // one 32-bit lane offset
-  const uint8_t* const abase0 = band + ((p.ch0 + 1) << 4);
+  const uint8_t* const abase0 = band + ((p.ch0 + p.js) << 4);
   const uint8_t* const rbase0 = abase0 + p.ref_off;
   // f0: first item of the double batch (warp-uniform)
   auto issue_dbl = [&](uint32_t f0, RawItem& x0, RawItem& x1) {
@@ -666,8 +688,8 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
     const uint32_t i0 = mbeg + b0 * 64;
     const uint32_t i1 = mbeg + min(m_items, (b0 + nbat) * 64) - 1;
     const uint32_t r0 = fast_div(i0, p.ni_mul, p.ni_shr), r1 = fast_div(i1, p.ni_mul, p.ni_shr);
-    long long a0 = (long long)r0 * pitch + ((p.ch0 + 1 + (i0 - r0 * ni)) << 4) + p.ref_off;
-    long long a1 = (long long)r1 * pitch + ((p.ch0 + 1 + (i1 - r1 * ni)) << 4) + p.ref_off + 32;
+    long long a0 = (long long)r0 * pitch + ((p.ch0 + p.js + (i0 - r0 * ni)) << 4) + p.ref_off;
+    long long a1 = (long long)r1 * pitch + ((p.ch0 + p.js + (i1 - r1 * ni)) << 4) + p.ref_off + 32;
     a0 = max(a0, 0ll) & ~15ll;
     a1 = min(a1, (long long)p.buf_bytes);
     if (a1 > a0) prefetch_l2(band + a0, (uint32_t)min(a1 - a0, 1ll << 20) & ~15u);
@@ -779,11 +801,12 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
         const uint32_t e = ebeg + local;
         row = fast_div(e, p.ne_mul, p.ne_shr);
         const uint32_t r = e - row * ne;
-        j = ni ? (r ? nch - 1 : 0u) : r;
+        // edge segments of a row: [0, js) and [js + ni, nch)
+        j = (ni && r >= (uint32_t)p.js) ? r + ni : r;
       } else {
         const uint32_t f = tail0 + (local - e_items);
         row = fast_div(f, p.ni_mul, p.ni_shr);
-        j = 1 + (f - row * ni);
+        j = p.js + (f - row * ni);
       }
       RawItem it;
       issue_item<KSEL>(p, band, row, j, local < n_work, it);
