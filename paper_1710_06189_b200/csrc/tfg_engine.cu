@@ -225,6 +225,22 @@ VoteKernel tfg_pick_vote_q1(int strat, int ksel);
 VoteKernel tfg_pick_vote_q2(int strat, int ksel);
 VoteKernel tfg_pick_vote_q3(int strat, int ksel);
 namespace {
+using JobsKernel = void (*)(const tfg::VoteJobs);
+}  // namespace
+JobsKernel tfg_pick_jobs_q0(int strat);
+JobsKernel tfg_pick_jobs_q1(int strat);
+JobsKernel tfg_pick_jobs_q2(int strat);
+JobsKernel tfg_pick_jobs_q3(int strat);
+namespace {
+JobsKernel pick_jobs(int quant, int strat) {
+  switch (quant) {
+    case tfg::Q_NONE: return tfg_pick_jobs_q0(strat);
+    case tfg::Q_CLAMP: return tfg_pick_jobs_q1(strat);
+    case tfg::Q_SHIFT: return tfg_pick_jobs_q2(strat);
+    default: return tfg_pick_jobs_q3(strat);
+  }
+}
+
 VoteKernel pick_vote(int quant, int strat, int ksel) {
   switch (quant) {
     case tfg::Q_NONE: return tfg_pick_vote_q0(strat, ksel);
@@ -287,7 +303,8 @@ std::mutex g_kinfo_mu;
 std::vector<VoteKernel> g_kopted;
 std::vector<std::pair<std::pair<VoteKernel, size_t>, int>> g_kocc;
 
-int occupancy_for(VoteKernel fn, size_t smem) {
+int occupancy_for(const void* fn_ptr, size_t smem) {
+  VoteKernel fn = reinterpret_cast<VoteKernel>(const_cast<void*>(fn_ptr));
   std::lock_guard<std::mutex> lk(g_kinfo_mu);
   for (auto& e : g_kocc)
     if (e.first.first == fn && e.first.second == smem) return e.second;
@@ -456,21 +473,26 @@ struct ScratchOrder {
   }
 };
 
-// Enqueue the vote of one (d, theta) for n_bands bands into d_glcm (added).
-void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
-                 size_t band_stride, int n_bands, size_t row_end, int pixel_levels, int levels,
-                 int distance, int angle, unsigned flags, unsigned long long* d_glcm, cudaStream_t s) {
+// Geometry, quantiser and layout of one (d, theta) vote (launch_vote and
+// launch_vote_jobs share it).
+struct VotePrep {
+  VoteGeometry g;
+  int quant = 0;
+};
+VotePrep prepare_vote(const uint8_t* d_img, size_t width, size_t height, size_t pitch, size_t band_stride,
+                      int n_bands, size_t row_end, int pixel_levels, int levels, int distance, int angle,
+                      unsigned flags, unsigned long long* d_glcm) {
   const bool aligned = align_interior_enabled() && reinterpret_cast<uintptr_t>(d_img) % 128 == 0 &&
                        (n_bands == 1 || band_stride % 128 == 0);
-  VoteGeometry g = make_geometry(width, height, pitch, row_end, levels, pixel_levels, distance, angle, aligned);
-  if (g.empty) return;
-  tfg::VoteParams& p = g.p;
+  VotePrep v;
+  v.g = make_geometry(width, height, pitch, row_end, levels, pixel_levels, distance, angle, aligned);
+  tfg::VoteParams& p = v.g.p;
   p.img = d_img;
   p.band_stride = band_stride;
   p.glcm = d_glcm;
   int lg = 0;
-  const int quant = quant_mode(pixel_levels, levels, &p.qmask, &p.qshift, &lg);
-  if (quant == tfg::Q_SHIFT && !(flags & TFG_SCHEME_GLOBAL)) {
+  v.quant = quant_mode(pixel_levels, levels, &p.qmask, &p.qshift, &lg);
+  if (v.quant == tfg::Q_SHIFT && !(flags & TFG_SCHEME_GLOBAL)) {
     // the scaled side of a layout: ((v >> s) & m) << sc == (v >> (s - sc)) & (m << sc); s >= sc
     // holds because each layout is only used for L <= 2^(8 - sc).
     const int strat = pick_strategy(levels, flags);
@@ -480,6 +502,82 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
     p.rshift = p.sbits + (ref_scaled ? p.qshift_scaled : p.qshift);
     p.rmask = ref_scaled ? (p.qmask << tfg::strat_scale(strat)) : p.qmask;
   }
+  return v;
+}
+
+// Multi-job launches (glcm_vote_jobs_kernel); TEXFORGE_JOBS=0 launches every
+// (d, theta) on its own for A/B timing.
+bool jobs_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("TEXFORGE_JOBS");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// Enqueues n (d, theta) votes of the same image (or band batch) as ONE
+// glcm_vote_jobs_kernel launch: job t adds into d_counts + t * per_dt (band
+// b at + b * L^2). Only for the layouts without per-CTA partials (L <= 64);
+// returns false when it does not apply and the caller launches per (d, theta).
+bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
+                      size_t band_stride, int n_bands, size_t row_end, int pixel_levels, int levels,
+                      const int* distances, const int* angles, int n, unsigned flags, unsigned long long* d_counts,
+                      size_t per_dt, cudaStream_t s) {
+  if (n < 2 || n > tfg::kMaxJobs || (flags & TFG_SCHEME_GLOBAL) || (size_t)levels * levels > 4096 ||
+      !jobs_enabled())
+    return false;
+  const int strat = pick_strategy(levels, flags);
+  uint32_t qm = 0;
+  int qs = 0;
+  const int quant = quant_mode(pixel_levels, levels, &qm, &qs);
+  JobsKernel fn = pick_jobs(quant, strat);
+  if (!fn) return false;
+  const size_t words = hist_words_of(strat, levels);
+  const size_t smem = words * 4;
+  tfg::VoteJobs jp{};
+  int m = 0;
+  long long max_items = 0;
+  for (int t = 0; t < n; ++t) {
+    VotePrep v = prepare_vote(d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels, levels,
+                              distances[t], angles[t], flags, d_counts + (size_t)t * per_dt);
+    if (v.g.empty) continue;
+    v.g.p.hist_words = (int)words;
+    jp.job[m] = v.g.p;
+    jp.ksel[m] = v.g.ksel;
+    max_items = std::max(max_items, v.g.p.items);
+    ++m;
+  }
+  if (m == 0) return true;
+  const int bps = occupancy_for(reinterpret_cast<const void*>(fn), smem);
+  // one wave of CTAs split evenly over the (job, band) units (launch_vote's rule per unit)
+  const long long units = (long long)m * n_bands;
+  const long long slots = (long long)ctx->num_sms * bps;
+  long long per = units < slots ? std::max<long long>(1, slots / units)
+                                : std::max<long long>(1, (8 * slots + units - 1) / units);
+  per = std::max<long long>(1, std::min<long long>(per, (max_items + 2 * tfg::kThreads - 1) / (2 * tfg::kThreads)));
+  if (units > 65535) return false;
+  for (int j = 0; j < m; ++j) {
+    tfg::VoteParams& p = jp.job[j];
+    p.main_per_cta = ((p.pool_beg + per - 1) / per + 63) / 64 * 64;
+    p.edge_per_cta = (p.edge_items + per - 1) / per;
+  }
+  jp.nbands = n_bands;
+  fn<<<dim3((unsigned)per, (unsigned)units), tfg::kThreads, smem, s>>>(jp);
+  ck(cudaGetLastError(), "glcm_vote_jobs_kernel launch");
+  ctx->launches++;
+  return true;
+}
+
+// Enqueue the vote of one (d, theta) for n_bands bands into d_glcm (added).
+void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
+                 size_t band_stride, int n_bands, size_t row_end, int pixel_levels, int levels,
+                 int distance, int angle, unsigned flags, unsigned long long* d_glcm, cudaStream_t s) {
+  VotePrep v = prepare_vote(d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels, levels,
+                            distance, angle, flags, d_glcm);
+  VoteGeometry& g = v.g;
+  if (g.empty) return;
+  tfg::VoteParams& p = g.p;
+  const int quant = v.quant;
   const size_t cells = (size_t)levels * levels;
 
   if (flags & TFG_SCHEME_GLOBAL) {
@@ -497,7 +595,7 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   const size_t smem = words * 4;
   p.hist_words = (int)words;
   VoteKernel fn = pick_vote(quant, strat, g.ksel);
-  const int bps = occupancy_for(fn, smem);
+  const int bps = occupancy_for(reinterpret_cast<const void*>(fn), smem);
   // persistent-style grid: at most one wave of CTAs per band set, and no CTA
   // with less than one round of work.
   // One wave of persistent CTAs when the bands fit in it; otherwise ~8 waves,
@@ -779,9 +877,11 @@ void run_pipeline_specs(tfg_ctx* ctx, size_t width, const std::vector<uint64_t>&
     ck(cudaEventRecord(ctx->copied[sl], ctx->copy), "event record");
     ck(cudaStreamWaitEvent(ctx->exec, ctx->copied[sl], 0), "wait");
     if (pixel_levels == levels) launch_validate(ctx, dst, width, rows, pitch, 0, 1, levels, sync_err(ctx), ctx->exec);
-    for (int t = 0; t < n_dt; ++t)
-      launch_vote(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, levels, distances[t],
-                  angles[t], flags, d_acc + bnd * acc_band_stride + (size_t)t * levels * levels, ctx->exec);
+    if (!launch_vote_jobs(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, levels, distances,
+                          angles, n_dt, flags, d_acc + bnd * acc_band_stride, (size_t)levels * levels, ctx->exec))
+      for (int t = 0; t < n_dt; ++t)
+        launch_vote(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, levels, distances[t],
+                    angles[t], flags, d_acc + bnd * acc_band_stride + (size_t)t * levels * levels, ctx->exec);
     ck(cudaEventRecord(ctx->consumed[sl], ctx->exec), "event record");
     if (band_done && i == k - 1) band_done(bnd);
     if (sequential) ck(cudaStreamSynchronize(ctx->exec), "stream sync");
@@ -1125,7 +1225,10 @@ int glcm_impl_locked(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t heigh
     }
     if (pixel_levels == levels)
       launch_validate(ctx, d_img, width, height, dpitch, dstride, (int)n_bands, levels, sync_err(ctx), s);
-    for (int t = 0; t < n_dt; ++t) {
+    const bool jobs = n_bands == 1 && launch_vote_jobs(ctx, d_img, width, height, dpitch, dstride, 1, owned_rows,
+                                                       pixel_levels, levels, distances, angles_deg, n_dt, flags,
+                                                       d_acc, cells, s);
+    for (int t = 0; t < n_dt && !jobs; ++t) {
       // bands are batched in one launch (blockIdx.y = band); outputs band-major
       // [band][dt][cell]: launch per dt writing with a band stride of n_dt*cells.
       if (n_dt == 1) {
@@ -1500,6 +1603,11 @@ int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
     if (pixel_levels == levels)
       launch_validate(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, levels, ctx->d_err, s);
     const size_t per_dt = n_bands * (size_t)levels * levels;
+    // every (d, theta) of an L <= 64 image or band batch in one launch
+    if (launch_vote_jobs(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, row_end, pixel_levels, levels,
+                         distances, angles_deg, n_dt, flags, reinterpret_cast<unsigned long long*>(d_counts), per_dt,
+                         s))
+      return;
     // L <= 64 launches share no scratch (direct u64 atomics, per-CTA smem
     // tickets): fork them over the context's aux streams so one GLCM's
     // prologue/epilogue and tail overlap another's votes (small images are

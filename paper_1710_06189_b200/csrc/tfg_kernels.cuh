@@ -558,14 +558,15 @@ __device__ __forceinline__ void reduce_partials_slice(const VoteParams& p, uint3
 //  * edge pass — the first and last segment of every row (or every segment
 //    of a narrow image), with per-lane guarded loads and valid-anchor masks.
 // There is no barrier in either loop (PACKED16 included: see kDrainBit).
+// vote_cta: the work of CTA `cta` of band `band_idx` (glcm_vote_kernel: the
+// block's x and y; glcm_vote_jobs_kernel: one job's share of the grid).
 template <int QUANT, int STRAT, int KSEL>
-__global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams p) {
+__device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta, const int band_idx) {
   extern __shared__ __align__(16) uint32_t hist[];
   __shared__ uint32_t s_ticket;
   constexpr uint32_t kWarps = kThreads / 32;
   const int tid = threadIdx.x;
   const uint32_t lane = tid & 31, warp = tid >> 5;
-  const int band_idx = blockIdx.y;
   const uint8_t* band = p.img + (unsigned long long)band_idx * p.band_stride;
   const uint32_t L = (uint32_t)p.levels;
   const int cells = p.levels * p.levels;
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
   };
 
   // ---------------- main pass: interior segments, 64 per double batch -------
-  const long long mbeg64 = (long long)blockIdx.x * p.main_per_cta;
+  const long long mbeg64 = (long long)cta * p.main_per_cta;
   const long long mend64 = min(mbeg64 + p.main_per_cta, p.pool_beg);
   const uint32_t mbeg = (uint32_t)mbeg64;
   const uint32_t m_items = mend64 > mbeg64 ? (uint32_t)(mend64 - mbeg64) : 0u;
@@ -787,7 +788,7 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
 
   // ---------------- edge pass: first/last segment of each row (or all) -----
   {
-    const long long ebeg64 = (long long)blockIdx.x * p.edge_per_cta;
+    const long long ebeg64 = (long long)cta * p.edge_per_cta;
     const long long eend64 = min(ebeg64 + p.edge_per_cta, p.edge_items);
     const uint32_t ebeg = (uint32_t)ebeg64;
     const uint32_t e_items = eend64 > ebeg64 ? (uint32_t)(eend64 - ebeg64) : 0u;
@@ -865,6 +866,42 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
 #pragma unroll 8
     for (int k = 0; k < RC; ++k) sum += hist[pos * RC + ((k + lane) & (RC - 1))];
     if (sum) atomicAdd(glcm + c, (unsigned long long)sum);
+  }
+}
+
+template <int QUANT, int STRAT, int KSEL>
+__global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams p) {
+  vote_cta<QUANT, STRAT, KSEL>(p, blockIdx.x, blockIdx.y);
+}
+
+// Several (d, theta) GLCMs of one image (or band batch) in ONE launch: grid
+// row y = job * nbands + band, x = the job's CTAs. Each job keeps its own
+// geometry; the reference-window variant (KSEL) is picked per CTA, so all
+// of an image's angles share one launch and its fixed costs (SURVEY.md §7
+// "small images are latency-bound"). Layouts without per-CTA partials
+// (L <= 64) only: those end in direct u64 atomics, not a grid barrier.
+constexpr int kMaxJobs = 8;
+struct VoteJobs {
+  VoteParams job[kMaxJobs];
+  int ksel[kMaxJobs];
+  int nbands;
+};
+
+template <int QUANT, int STRAT>
+__global__ void __launch_bounds__(kThreads, 1) glcm_vote_jobs_kernel(const __grid_constant__ VoteJobs jp) {
+  const int j = (int)blockIdx.y / jp.nbands;
+  const int band = (int)blockIdx.y - j * jp.nbands;
+  const VoteParams& p = jp.job[j];
+  switch (jp.ksel[j]) {
+    case 0: vote_cta<QUANT, STRAT, 0>(p, blockIdx.x, band); break;
+    case 1: vote_cta<QUANT, STRAT, 1>(p, blockIdx.x, band); break;
+    case 2: vote_cta<QUANT, STRAT, 2>(p, blockIdx.x, band); break;
+    case 3: vote_cta<QUANT, STRAT, 3>(p, blockIdx.x, band); break;
+    case 5: vote_cta<QUANT, STRAT, 5>(p, blockIdx.x, band); break;
+    case 6: vote_cta<QUANT, STRAT, 6>(p, blockIdx.x, band); break;
+    case 7: vote_cta<QUANT, STRAT, 7>(p, blockIdx.x, band); break;
+    case 8: vote_cta<QUANT, STRAT, 8>(p, blockIdx.x, band); break;
+    default: vote_cta<QUANT, STRAT, 4>(p, blockIdx.x, band); break;
   }
 }
 

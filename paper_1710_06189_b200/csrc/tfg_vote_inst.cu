@@ -39,3 +39,14 @@ VoteKernel TFG_CAT(tfg_pick_vote_q, TFG_QUANT)(int strat, int ksel) {
     default: return pick_k<Q, tfg::S_PACKED16>(ksel);
   }
 }
+
+using JobsKernel = void (*)(const tfg::VoteJobs);
+// the multi-job kernel of a layout without per-CTA partials (nullptr otherwise)
+JobsKernel TFG_CAT(tfg_pick_jobs_q, TFG_QUANT)(int strat) {
+  constexpr int Q = TFG_QUANT;
+  switch (strat) {
+    case tfg::S_COPIES32: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_COPIES32>;
+    case tfg::S_COPIES8: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_COPIES8>;
+    default: return nullptr;
+  }
+}

@@ -501,3 +501,24 @@ def test_pinned_counts_early_band_d2h(engine, levels, prequant):
                 want = (O.glcm_serial(imgs[b], w, h, levels, d, a) if prequant
                         else O.glcm_gray(imgs[b], w, h, levels, d, a))
                 assert np.array_equal(got[b, t].reshape(-1), want), (pinned_in, b, d, a)
+
+
+@pytest.mark.parametrize("levels,prequant", [(8, False), (37, False), (20, True), (64, False)])
+@pytest.mark.parametrize("w", [1031, 2048])
+def test_jobs_launch_every_window(engine, levels, prequant, w):
+    # glcm_vote_jobs_kernel: up to 8 (d, theta) of one image in ONE launch,
+    # the reference-window variant picked per CTA (every KSEL: d < 16 at
+    # 0 deg, aligned 16/32 deg-0 windows, 45/135 word shifts, 90 deg); 9
+    # pairs exceed kMaxJobs and take the per-(d, theta) launches
+    # (tfg_glcm_multi_async: test_multi_async_all_dts_bands_row_end).
+    h = 203
+    gray = tf.synth_noise(w, h, 7).pixels
+    px = O.quantize(gray, levels) if prequant else gray
+    src_levels = levels if prequant else 256
+    sets = [[(1, 0), (5, 0), (16, 0), (32, 0), (1, 45), (6, 45), (3, 90), (2, 135)],
+            [(1, 0), (2, 0), (3, 0), (4, 0), (1, 45), (1, 90), (1, 135), (9, 135), (12, 90)]]
+    for dts in sets:
+        got = engine.glcm(px, w, h, levels, dts, pixel_levels=src_levels)
+        for t, (d, a) in enumerate(dts):
+            want = O.glcm_gray(gray, w, h, levels, d, a)
+            assert np.array_equal(got[0, t].reshape(-1), want), (dts, d, a)

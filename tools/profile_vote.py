@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--strategy", type=int, default=0)
     ap.add_argument("--time", action="store_true")
+    ap.add_argument("--multi", action="store_true", help="one tfg_glcm_multi_async call for all --dts")
     a = ap.parse_args()
     n, levels = a.size, a.levels
     eng = tf.Engine(0)
@@ -39,6 +40,24 @@ def main():
     for kind in a.kinds.split(","):
         img = (tf.synth_noise if kind == "noise" else tf.synth_smooth)(n, n, 1).pixels
         dev = torch.from_numpy(img).cuda()
+        if a.multi:
+            nd = len(dts)
+            dd = (C.c_int * nd)(*[x[0] for x in dts])
+            aa = (C.c_int * nd)(*[x[1] for x in dts])
+            accm = torch.zeros(nd * levels * levels, dtype=torch.int64, device="cuda")
+            times = []
+            for r in range(a.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                L.check(lib.tfg_glcm_multi_async(eng.handle, C.c_void_p(dev.data_ptr()), n, n, n, n * n, 1, n, 256,
+                                                 levels, dd, aa, len(dts), L.strategy_flag(a.strategy),
+                                                 C.c_void_p(accm.data_ptr()), None))
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+            t = sorted(times)[len(times) // 2]
+            res[f"{kind} multi{nd}"] = {"ms": t, "GBps": nd * (n * n + levels * levels * 8) / (t / 1e3) / 1e9}
+            continue
         for d, th in dts:
             times = []
             for r in range(a.reps):
