@@ -30,7 +30,9 @@ def main():
     ap.add_argument("--strategy", type=int, default=0)
     ap.add_argument("--time", action="store_true")
     ap.add_argument("--multi", action="store_true", help="one tfg_glcm_multi_async call for all --dts")
+    ap.add_argument("--scheme1", action="store_true", help="K0: one global atomic per pair (Scheme 1 ablation)")
     a = ap.parse_args()
+    xflags = L.TFG_SCHEME_GLOBAL if a.scheme1 else 0
     n, levels = a.size, a.levels
     eng = tf.Engine(0)
     lib = L.load()
@@ -50,7 +52,7 @@ def main():
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 L.check(lib.tfg_glcm_multi_async(eng.handle, C.c_void_p(dev.data_ptr()), n, n, n, n * n, 1, n, 256,
-                                                 levels, dd, aa, len(dts), L.strategy_flag(a.strategy),
+                                                 levels, dd, aa, len(dts), L.strategy_flag(a.strategy) | xflags,
                                                  C.c_void_p(accm.data_ptr()), None))
                 e1.record()
                 torch.cuda.synchronize()
@@ -64,7 +66,7 @@ def main():
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 L.check(lib.tfg_glcm_async(eng.handle, C.c_void_p(dev.data_ptr()), n, n, n, n, 256, levels, d, th,
-                                           L.strategy_flag(a.strategy), C.c_void_p(acc.data_ptr()), None))
+                                           L.strategy_flag(a.strategy) | xflags, C.c_void_p(acc.data_ptr()), None))
                 e1.record()
                 torch.cuda.synchronize()
                 times.append(e0.elapsed_time(e1))
