@@ -533,7 +533,7 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
   JobsKernel fn = pick_jobs(quant, strat);
   if (!fn) return false;
   const size_t words = hist_words_of(strat, levels);
-  const size_t smem = words * 4;
+  const size_t smem = words * 4 + tfg::kTmaBytes;
   tfg::VoteJobs jp{};
   int m = 0;
   long long max_items = 0;
@@ -592,7 +592,7 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
 
   const int strat = pick_strategy(levels, flags);
   const size_t words = hist_words_of(strat, levels);
-  const size_t smem = words * 4;
+  const size_t smem = words * 4 + tfg::kTmaBytes;
   p.hist_words = (int)words;
   VoteKernel fn = pick_vote(quant, strat, g.ksel);
   const int bps = occupancy_for(reinterpret_cast<const void*>(fn), smem);

@@ -35,7 +35,13 @@ namespace tfg {
 #ifndef TFG_THREADS
 #define TFG_THREADS 1024
 #endif
+#ifndef TFG_TMA
+#define TFG_TMA 0
+#endif
 constexpr int kThreads = TFG_THREADS;  // threads per vote CTA (32 warps)
+// TFG_TMA: per-warp shared stages of the staged main pass behind the histogram
+// (2 stages x anchors + reference window, 2 mbarriers per warp)
+constexpr size_t kTmaBytes = TFG_TMA ? (size_t)(kThreads / 32) * (2 * 2 * (32 * 16 + 32) + 16) : 0;
 
 enum Quant : int {
   Q_NONE = 0,   // values used as-is (gray with L=256, or quantised with L=256)
@@ -338,6 +344,34 @@ __device__ __forceinline__ void prefetch_l2(const void* a, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
 }
 
+// mbarrier + bulk-copy (TMA engine) helpers for the staged main pass (TFG_TMA)
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TFG_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TFG_WAIT_%=;\n}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ uint4 lds16(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
 // ---------------------------------------------------------------------------
 // The three 16-byte loads of one item (anchor segment + the two aligned
 // segments that contain its reference bytes) and its valid-anchor mask.
@@ -502,6 +536,51 @@ __device__ __forceinline__ void reduce_partials_slice(const VoteParams& p, uint3
   const uint32_t w0 = min(words, blockIdx.x * slice), w1 = min(words, w0 + slice);
   if (w0 >= w1) return;
   const uint32_t* base = p.partials + (size_t)band_idx * nparts * words;
+  if constexpr (PACKED) {
+    // Thread t sums 4-word column group t % ng of the slice over partials
+    // t / ng, t / ng + groups, ...: 16-byte L2 loads, several in flight
+    // (the loop is unrolled). Field sums stay < 2^24 (<= 65535 per partial),
+    // so they meet in u32 shared-memory counters: [lo fields | hi fields].
+    // chunks of <= 4 * blockDim.x words (a grid of few CTAs has wide slices)
+    for (uint32_t c0 = w0; c0 < w1; c0 += 4 * blockDim.x) {
+      const uint32_t n = min(4 * blockDim.x, w1 - c0), ng = n / 4;  // words and slices are multiples of 4
+      uint32_t* acc32 = scratch;
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < 2 * n; i += blockDim.x) acc32[i] = 0;
+      __syncthreads();
+      const uint32_t groups = blockDim.x / ng;
+      const uint32_t cg = threadIdx.x % ng, g0 = threadIdx.x / ng;
+      if (g0 < groups) {
+        uint32_t lo0 = 0, lo1 = 0, lo2 = 0, lo3 = 0, hi0 = 0, hi1 = 0, hi2 = 0, hi3 = 0;
+        const uint4* src = reinterpret_cast<const uint4*>(base + c0) + cg;
+        const size_t stride4 = words / 4;
+#pragma unroll 4
+        for (uint32_t q = g0; q < nparts; q += groups) {
+          const uint4 v = __ldcg(src + q * stride4);
+          lo0 += v.x & 0xFFFFu; hi0 += v.x >> 16;
+          lo1 += v.y & 0xFFFFu; hi1 += v.y >> 16;
+          lo2 += v.z & 0xFFFFu; hi2 += v.z >> 16;
+          lo3 += v.w & 0xFFFFu; hi3 += v.w >> 16;
+        }
+        uint32_t* a = acc32 + 4 * cg;
+        if (lo0) atomicAdd(a + 0, lo0);
+        if (lo1) atomicAdd(a + 1, lo1);
+        if (lo2) atomicAdd(a + 2, lo2);
+        if (lo3) atomicAdd(a + 3, lo3);
+        if (hi0) atomicAdd(a + n + 0, hi0);
+        if (hi1) atomicAdd(a + n + 1, hi1);
+        if (hi2) atomicAdd(a + n + 2, hi2);
+        if (hi3) atomicAdd(a + n + 3, hi3);
+      }
+      __syncthreads();
+      for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
+        const uint32_t w = c0 + c, a = w & 0xFFu, b = w >> 8;
+        if (acc32[c]) atomicAdd(glcm + b * L + a, (unsigned long long)acc32[c]);
+        if (acc32[n + c]) atomicAdd(glcm + (b + 128u) * L + a, (unsigned long long)acc32[n + c]);
+      }
+    }
+    return;
+  }
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(scratch);  // [ncol][2]
   // columns in chunks of at most blockDim.x; thread t: column t % ncol,
   // partials t / ncol, t / ncol + groups, ...
@@ -711,6 +790,141 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
     return __shfl_sync(0xffffffffu, tn, 0);
   };
 
+#if TFG_TMA
+  // ---- staged main pass: the TMA engine (cp.async.bulk) copies each batch
+  // of 32 interior segments (+ its reference window) into the warp's shared
+  // stage; two stages per warp, one loading while the other is voted. The
+  // register ring of the LDG pass is gone; each lane reads its item with
+  // ld.shared. Batches come in pairs from the per-CTA tickets (one double
+  // batch per grab), then four double batches per grab from the shared pool.
+  {
+    constexpr uint32_t kStageA = 32 * 16 + 32;                // anchors + the segment after each row piece
+    constexpr bool kRef = !ksel_c0_is_anchor<KSEL>();         // separate reference rows (theta != 0 or d >= 16)
+    constexpr uint32_t kStage = kRef ? 2 * kStageA : kStageA;
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(hist + p.hist_words)) + warp * 2 * kStage;
+    const uint32_t bars = static_cast<uint32_t>(__cvta_generic_to_shared(hist + p.hist_words)) +
+                          kWarps * 2 * kStage + warp * 16;
+    if (lane == 0) {
+      mbar_init(bars, 1);
+      mbar_init(bars + 8, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid == 0) s_ticket = kWarps;
+    __syncthreads();  // histogram zeroed, ticket counter set, barriers initialised
+    // batch generator: single batches of 32 items, two per double batch
+    uint32_t q_base = mbeg + warp * 64, q_left = warp < n_full_dbl ? 2u : 0u;
+    bool own = true;
+    constexpr uint32_t kNone = 0xFFFFFFFFu;
+    auto next_batch = [&]() -> uint32_t {
+      if (q_left == 0) {
+        if (own) {
+          uint32_t tn = 0;
+          if (lane == 0) {
+            asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(tn) : "r"(ticket_addr) : "memory");
+            if ((tn & (kSpan - 1)) == 0) prefetch_span(tn + kAhead, kSpan);
+          }
+          tn = __shfl_sync(0xffffffffu, tn, 0);
+          if (tn < n_full_dbl) {
+            q_base = mbeg + tn * 64;
+            q_left = 2;
+          } else {
+            own = false;
+          }
+        }
+        if (!own) {
+          if constexpr (STRAT == S_PACKED16 || STRAT == S_COPY1) {
+            uint32_t g = kNone;
+            if (lane == 0 && p.pool_ctr) {
+              const uint32_t tp = atomicAdd(p.pool_ctr + band_idx, 4u);
+              if (tp < p.pool_dbl) g = (uint32_t)p.pool_beg + tp * 64;
+            }
+            g = __shfl_sync(0xffffffffu, g, 0);
+            if (g == kNone) return kNone;
+            q_base = g;
+            q_left = 8;
+          } else {
+            return kNone;
+          }
+        }
+      }
+      const uint32_t b = q_base;
+      q_base += 32;
+      --q_left;
+      return b;
+    };
+    // items [f0, f0 + 32): n1 of them in row0, the rest at the start of row0 + 1
+    auto pieces = [&](uint32_t f0, uint32_t& row0, uint32_t& jj0, uint32_t& n1) {
+      row0 = fast_div(f0, p.ni_mul, p.ni_shr);
+      jj0 = f0 - row0 * ni;
+      n1 = min(32u, ni - jj0);
+    };
+    auto issue = [&](uint32_t st, uint32_t f0) {  // lane 0
+      uint32_t row0, jj0, n1;
+      pieces(f0, row0, jj0, n1);
+      const uint32_t dstA = sbase + st * kStage, bar = bars + st * 8;
+      const uint8_t* a1 = abase0 + (unsigned long long)row0 * pitch + (jj0 << 4);
+      const uint32_t b1 = n1 * 16 + 16;
+      const uint32_t n2 = 32 - n1;
+      const uint32_t b2 = n2 ? n2 * 16 + 16 : 0u;
+      constexpr uint32_t kRefLess = ksel_needs_c1<KSEL>() ? 0u : 16u;  // reference pieces skip the extra segment
+      mbar_expect_tx(bar, kRef ? 2 * (b1 + b2) - kRefLess * (n2 ? 2u : 1u) : b1 + b2);
+      bulk_g2s(dstA, a1, b1, bar);
+      if (n2) bulk_g2s(dstA + b1, abase0 + (unsigned long long)(row0 + 1) * pitch, b2, bar);
+      if constexpr (kRef) {
+        // reference rows: the c0 segments (+ the c1 after the last one when
+        // the window is unaligned); the same bytes the LDG pass reads
+        constexpr uint32_t kX = ksel_needs_c1<KSEL>() ? 16u : 0u;
+        bulk_g2s(dstA + kStageA, a1 + p.ref_off, b1 - 16 + kX, bar);
+        if (n2)
+          bulk_g2s(dstA + kStageA + b1, abase0 + (unsigned long long)(row0 + 1) * pitch + p.ref_off, b2 - 16 + kX, bar);
+      }
+    };
+    uint32_t fb0 = next_batch();
+    uint32_t fb1 = fb0 == kNone ? kNone : next_batch();
+    if (lane == 0) {
+      if (fb0 != kNone) issue(0, fb0);
+      if (fb1 != kNone) issue(1, fb1);
+    }
+    uint32_t ph0 = 0, ph1 = 0;
+    // vote the batch in stage `st`, then refill the stage with the next batch
+    auto step = [&](const uint32_t st, uint32_t& fb, uint32_t& ph) {
+      mbar_wait(bars + st * 8, ph);
+      ph ^= 1u;
+      uint32_t row0, jj0, n1;
+      pieces(fb, row0, jj0, n1);
+      const uint32_t off = sbase + st * kStage + lane * 16 + (lane >= n1 ? 16u : 0u);
+      RawItem it;
+      it.mask = 0xFFFFu;
+      it.a = lds16(off);
+      if constexpr (kRef) {
+        it.c0 = lds16(off + kStageA);
+        if constexpr (ksel_needs_c1<KSEL>()) it.c1 = lds16(off + kStageA + 16);
+      } else {
+        it.c1 = lds16(off + 16);
+      }
+      __syncwarp();  // every lane has read the stage before the copy engine refills it
+      fb = next_batch();
+      if (lane == 0 && fb != kNone) {
+        fence_proxy_async();
+        issue(st, fb);
+      }
+      vote_full(it);
+    };
+    for (;;) {
+      if (fb0 == kNone) break;
+      step(0, fb0, ph0);
+      if (fb1 == kNone) break;
+      step(1, fb1, ph1);
+    }
+    if (lane == 0) {
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bars) : "memory");
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bars + 8) : "memory");
+    }
+  }
+  if (false) {
+#else
+  {
+#endif
   RawItem a0, a1, b0i, b1i;
   uint32_t ta = 2 * warp, tb = 2 * warp + 1;
   if (ta < n_full_dbl) issue_dbl(mbeg + ta * 64, a0, a1);
@@ -785,6 +999,8 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
       }
     }
   }
+
+  }  // LDG main pass
 
   // ---------------- edge pass: first/last segment of each row (or all) -----
   {
