@@ -537,7 +537,9 @@ def run_engine(args, wl):
         dev[kind] = t
     torch.cuda.synchronize()
 
-    jobs = [(L, kind, d, a) for L in plan.levels_list for kind in plan.kinds for (d, a) in plan.dts]
+    # input-major: every GLCM of one input is contiguous in `acc`, so one
+    # tfg_glcm_jobs_async call per input covers all its (L, d, theta)
+    jobs = [(L, kind, d, a) for kind in plan.kinds for L in plan.levels_list for (d, a) in plan.dts]
     cells = {L: L * L for L in plan.levels_list}
     out_off, o = [], 0
     for (L, _k, _d, _a) in jobs:
@@ -552,29 +554,30 @@ def run_engine(args, wl):
     launches = []
     record = {"on": False}
 
-    # timed steps: one engine call per (L, input) with every (d, theta)
-    # (tfg_glcm_multi_async); the roofline pass below times single launches
-    groups = []
+    # timed steps: one engine call per input with every (L, d, theta) of it
+    # (tfg_glcm_jobs_async); the roofline pass below times single launches
+    groups = []  # (kind, first job, [(L, d, theta)])
     for j, (L, kind, d, a) in enumerate(jobs):
-        if groups and groups[-1][0] == (L, kind):
-            groups[-1][2].append((d, a))
+        if groups and groups[-1][0] == kind:
+            groups[-1][2].append((L, d, a))
         else:
-            groups.append(((L, kind), j, [(d, a)]))
+            groups.append((kind, j, [(L, d, a)]))
     gargs = []
-    for (L, kind), j0, dts_g in groups:
-        n = len(dts_g)
-        gargs.append((L, kind, out_off[j0], n, (C.c_int * n)(*[x[0] for x in dts_g]),
-                      (C.c_int * n)(*[x[1] for x in dts_g])))
+    for kind, j0, g in groups:
+        n = len(g)
+        gargs.append((kind, out_off[j0], n, (C.c_int * n)(*[x[0] for x in g]), (C.c_int * n)(*[x[1] for x in g]),
+                      (C.c_int * n)(*[x[2] for x in g])))
 
     cur = {"s": sptr}  # stream the engine calls enqueue on (the capture stream while recording a graph)
 
     def vote_grouped():
-        for L, kind, off, n, dd, aa in gargs:
+        # one engine call per input: every (L, d, theta) of it (tfg_glcm_jobs_async)
+        for kind, off, n, ll, dd, aa in gargs:
             bands = plan.bands if plan.layout == "bands" else 1
             rows = plan.height if plan.layout == "bands" else buf_rows[kind]
-            rc = lib.tfg_glcm_multi_async(eng.handle, C.c_void_p(dev[kind].data_ptr()), W, rows, W, W * rows, bands,
-                                          plan.owned if plan.layout != "bands" else rows, 256, L, dd, aa, n, 0,
-                                          C.c_void_p(acc.data_ptr() + off * 8), cur["s"])
+            rc = lib.tfg_glcm_jobs_async(eng.handle, C.c_void_p(dev[kind].data_ptr()), W, rows, W, W * rows, bands,
+                                         plan.owned if plan.layout != "bands" else rows, 256, ll, dd, aa, n, 0,
+                                         C.c_void_p(acc.data_ptr() + off * 8), cur["s"])
             if rc:
                 Lb.check(rc)
 

@@ -237,6 +237,18 @@ int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
                          const int* distances, const int* angles_deg, int n_dt, unsigned flags, uint64_t* d_counts,
                          void* stream);
 
+/*
+ * Several GLCMs of one device image (or band batch) with per-job levels and
+ * (d, theta): equivalent to n_jobs tfg_glcm_async calls, job t's counts at
+ * d_counts + sum_{u<t} n_bands * levels[u]^2 (band-major). Jobs that share a
+ * kernel instantiation (L <= 64, same quantiser and layout) run as one
+ * launch of up to 8 jobs. Stream-ordered like tfg_glcm_multi_async.
+ */
+int tfg_glcm_jobs_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t height, size_t pitch,
+                        size_t band_stride, size_t n_bands, size_t row_end, int pixel_levels, const int* levels,
+                        const int* distances, const int* angles_deg, int n_jobs, unsigned flags, uint64_t* d_counts,
+                        void* stream);
+
 /* Device post-processing on `stream`: symmetrize (in place allowed? no: out != in). */
 int tfg_post_async(tfg_ctx* ctx, const uint64_t* d_counts, int levels, unsigned flags,
                    uint64_t* d_sym_out, double* d_probs_out, double* d_feats_out, void* stream);

@@ -84,6 +84,8 @@ SIGNATURES = [
                                        C.c_int, C.c_uint, C.c_void_p, C.c_void_p]),
     ("tfg_glcm_multi_async", C.c_int, [C.c_void_p, C.c_void_p, _sz, _sz, _sz, _sz, _sz, _sz, C.c_int, C.c_int, _ip,
                                        _ip, C.c_int, C.c_uint, C.c_void_p, C.c_void_p]),
+    ("tfg_glcm_jobs_async", C.c_int, [C.c_void_p, C.c_void_p, _sz, _sz, _sz, _sz, _sz, _sz, C.c_int, _ip, _ip, _ip,
+                                      C.c_int, C.c_uint, C.c_void_p, C.c_void_p]),
     ("tfg_post_async", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p]),
     ("tfg_check_async_errors", C.c_int, [C.c_void_p]),

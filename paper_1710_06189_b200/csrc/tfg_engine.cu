@@ -520,28 +520,35 @@ bool jobs_enabled() {
 // b at + b * L^2). Only for the layouts without per-CTA partials (L <= 64);
 // returns false when it does not apply and the caller launches per (d, theta).
 bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
-                      size_t band_stride, int n_bands, size_t row_end, int pixel_levels, int levels,
-                      const int* distances, const int* angles, int n, unsigned flags, unsigned long long* d_counts,
-                      size_t per_dt, cudaStream_t s) {
-  if (n < 2 || n > tfg::kMaxJobs || (flags & TFG_SCHEME_GLOBAL) || (size_t)levels * levels > 4096 ||
-      !jobs_enabled())
-    return false;
-  const int strat = pick_strategy(levels, flags);
-  uint32_t qm = 0;
-  int qs = 0;
-  const int quant = quant_mode(pixel_levels, levels, &qm, &qs);
+                      size_t band_stride, int n_bands, size_t row_end, int pixel_levels, const int* levels,
+                      const int* distances, const int* angles, unsigned long long* const* outs, int n,
+                      unsigned flags, cudaStream_t s) {
+  if (n < 2 || n > tfg::kMaxJobs || (flags & TFG_SCHEME_GLOBAL) || !jobs_enabled()) return false;
+  // one kernel instantiation: every job needs the same quantiser and layout
+  int quant = -1, strat = -1;
+  size_t words = 0;
+  for (int t = 0; t < n; ++t) {
+    if ((size_t)levels[t] * levels[t] > 4096) return false;
+    uint32_t qm = 0;
+    int qs = 0;
+    const int q = quant_mode(pixel_levels, levels[t], &qm, &qs);
+    const int st = pick_strategy(levels[t], flags);
+    if ((quant >= 0 && q != quant) || (strat >= 0 && st != strat)) return false;
+    quant = q;
+    strat = st;
+    words = std::max(words, hist_words_of(st, levels[t]));
+  }
   JobsKernel fn = pick_jobs(quant, strat);
   if (!fn) return false;
-  const size_t words = hist_words_of(strat, levels);
   const size_t smem = words * 4 + tfg::kTmaBytes;
   tfg::VoteJobs jp{};
   int m = 0;
   long long max_items = 0;
   for (int t = 0; t < n; ++t) {
-    VotePrep v = prepare_vote(d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels, levels,
-                              distances[t], angles[t], flags, d_counts + (size_t)t * per_dt);
+    VotePrep v = prepare_vote(d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels, levels[t],
+                              distances[t], angles[t], flags, outs[t]);
     if (v.g.empty) continue;
-    v.g.p.hist_words = (int)words;
+    v.g.p.hist_words = (int)hist_words_of(strat, levels[t]);
     jp.job[m] = v.g.p;
     jp.ksel[m] = v.g.ksel;
     max_items = std::max(max_items, v.g.p.items);
@@ -566,6 +573,22 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
   ck(cudaGetLastError(), "glcm_vote_jobs_kernel launch");
   ctx->launches++;
   return true;
+}
+
+// The common case: n (d, theta) at one L, job t adding into d_counts + t * per_dt.
+bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
+                      size_t band_stride, int n_bands, size_t row_end, int pixel_levels, int levels,
+                      const int* distances, const int* angles, int n, unsigned flags, unsigned long long* d_counts,
+                      size_t per_dt, cudaStream_t s) {
+  if (n < 2 || n > tfg::kMaxJobs) return false;
+  int lv[tfg::kMaxJobs];
+  unsigned long long* outs[tfg::kMaxJobs];
+  for (int t = 0; t < n; ++t) {
+    lv[t] = levels;
+    outs[t] = d_counts + (size_t)t * per_dt;
+  }
+  return launch_vote_jobs(ctx, d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels, lv, distances,
+                          angles, outs, n, flags, s);
 }
 
 // Enqueue the vote of one (d, theta) for n_bands bands into d_glcm (added).
@@ -1630,6 +1653,55 @@ int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
         ck(cudaEventRecord(ctx->join_ev[i], ctx->aux[i]), "event record");
         ck(cudaStreamWaitEvent(s, ctx->join_ev[i], 0), "wait");
       }
+    }
+  });
+}
+
+int tfg_glcm_jobs_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t height, size_t pitch,
+                        size_t band_stride, size_t n_bands, size_t row_end, int pixel_levels, const int* levels,
+                        const int* distances, const int* angles_deg, int n_jobs, unsigned flags, uint64_t* d_counts,
+                        void* stream) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded([&] {
+    if (n_jobs < 1 || !levels || !distances || !angles_deg) fail(TFG_INVALID_ARGUMENT, "glcm: need at least one job");
+    for (int t = 0; t < n_jobs; ++t) {
+      check_levels(levels[t], "glcm");
+      check_pixel_levels(pixel_levels, levels[t]);
+      check_angle(angles_deg[t]);
+      if (distances[t] < 1 || (size_t)distances[t] >= width)
+        fail(TFG_INVALID_ARGUMENT, "glcm: degenerate geometry (d must be in [1, min(width, height)))");
+    }
+    if ((reinterpret_cast<uintptr_t>(d_px) & 15) || (pitch % 16) || pitch < width || (n_bands > 1 && band_stride % 16))
+      fail(TFG_INVALID_ARGUMENT, "glcm_async: device image must be 16-byte aligned with pitch % 16 == 0");
+    if (n_bands < 1 || n_bands > 65535) fail(TFG_INVALID_ARGUMENT, "glcm: band count must be in [1, 65535]");
+    if (n_bands > 1 && band_stride < pitch * height) fail(TFG_INVALID_ARGUMENT, "glcm: bands overlap");
+    if (row_end > height) fail(TFG_INVALID_ARGUMENT, "glcm_async: row_end > height");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (pixel_levels < 256) {
+      // pre-quantised input: every job has levels == pixel_levels (check_pixel_levels)
+      launch_validate(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, pixel_levels, ctx->d_err, s);
+    }
+    std::vector<unsigned long long*> outs((size_t)n_jobs);
+    size_t off = 0;
+    for (int t = 0; t < n_jobs; ++t) {
+      outs[t] = reinterpret_cast<unsigned long long*>(d_counts) + off;
+      off += n_bands * (size_t)levels[t] * levels[t];
+    }
+    // runs of jobs that share a kernel instantiation go out as one launch of
+    // up to kMaxJobs; the rest one launch per job (ordered on `s`)
+    int t = 0;
+    while (t < n_jobs) {
+      int n = std::min(n_jobs - t, tfg::kMaxJobs);
+      while (n > 1 && !launch_vote_jobs(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, row_end,
+                                         pixel_levels, levels + t, distances + t, angles_deg + t, outs.data() + t, n,
+                                         flags, s))
+        --n;
+      if (n == 1)
+        launch_vote(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, row_end, pixel_levels, levels[t],
+                    distances[t], angles_deg[t], flags, outs[t], s);
+      t += n;
     }
   });
 }

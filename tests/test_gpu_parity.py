@@ -522,3 +522,39 @@ def test_jobs_launch_every_window(engine, levels, prequant, w):
         for t, (d, a) in enumerate(dts):
             want = O.glcm_gray(gray, w, h, levels, d, a)
             assert np.array_equal(got[0, t].reshape(-1), want), (dts, d, a)
+
+
+@pytest.mark.parametrize("nb", [1, 3])
+def test_jobs_async_mixed_levels(engine, nb):
+    # tfg_glcm_jobs_async: per-job (L, d, theta) of one device image / band
+    # batch; runs sharing a kernel instantiation (L=16 and 32: COPIES32) go
+    # out as one launch, L=64 (COPIES8) and L=256 (PACKED16) on their own
+    import torch
+    w, h = 700, 130
+    imgs = [tf.synth_noise(w, h, 60 + b).pixels if b % 2 == 0 else tf.synth_smooth(w, h, 60 + b).pixels
+            for b in range(nb)]
+    pitch = 704
+    buf = np.zeros((nb, h, pitch), np.uint8)
+    for b in range(nb):
+        buf[b, :, :w] = imgs[b].reshape(h, w)
+    dev = torch.from_numpy(buf).cuda()
+    jobs = [(16, 1, 0), (16, 2, 45), (32, 1, 90), (32, 3, 135), (32, 1, 0), (64, 1, 45), (256, 2, 90), (16, 4, 0),
+            (32, 2, 0), (16, 1, 135)]
+    n = len(jobs)
+    lv = (C.c_int * n)(*[j[0] for j in jobs])
+    dd = (C.c_int * n)(*[j[1] for j in jobs])
+    aa = (C.c_int * n)(*[j[2] for j in jobs])
+    total = sum(nb * j[0] * j[0] for j in jobs)
+    out = torch.zeros(total, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+    L.check(engine._lib.tfg_glcm_jobs_async(engine.handle, C.c_void_p(dev.data_ptr()), w, h, pitch, pitch * h, nb, h,
+                                            256, lv, dd, aa, n, 0, C.c_void_p(out.data_ptr()),
+                                            C.c_void_p(s.cuda_stream)))
+    got = out.cpu().numpy().view(np.uint64)
+    off = 0
+    for (levels, d, a) in jobs:
+        cells = levels * levels
+        for b in range(nb):
+            want = O.glcm_gray(imgs[b], w, h, levels, d, a)
+            assert np.array_equal(got[off + b * cells: off + (b + 1) * cells], want), (levels, d, a, b)
+        off += nb * cells
