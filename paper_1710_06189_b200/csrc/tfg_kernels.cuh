@@ -961,41 +961,51 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
   }
 
   // Shared tail pool (cooperative launches): once its own range is done, a
-  // warp takes four double batches [g, g + 256) per grab from the band's
-  // global counter (the pool is a whole number of grabs). The counter only
-  // grows, so the first empty grab ends the warp's main pass. Only the
-  // layouts with per-CTA partials (L > 64) end at a grid barrier, so only
-  // they carry this loop.
+  // warp takes TFG_POOL_GRAB double batches per grab from the band's global
+  // counter (4: grabs of 1 or 2 measured 11% / 1% slower, contention on the
+  // one counter). The counter only grows, so an empty grab ends that ring
+  // slot. Only the layouts with per-CTA partials (L > 64) end at
+  // a grid barrier, so only they carry this loop.
+#ifndef TFG_POOL_GRAB
+#define TFG_POOL_GRAB 4
+#endif
   if constexpr (STRAT == S_PACKED16 || STRAT == S_COPY1) {
     if (p.pool_ctr) {
-      constexpr uint32_t kNone = 0xFFFFFFFFu;
-      auto grab_pool = [&]() -> uint32_t {
-        uint32_t g = kNone;
-        if (lane == 0) {
-          const uint32_t tp = atomicAdd(p.pool_ctr + band_idx, 4u);
-          if (tp < p.pool_dbl) g = (uint32_t)p.pool_beg + tp * 64;
+      constexpr uint32_t kNone = 0xFFFFFFFFu, kGrab = TFG_POOL_GRAB;
+      uint32_t gbase = 0, gleft = 0;
+      auto grab_pool = [&]() -> uint32_t {  // next pool double batch (warp-uniform) or kNone
+        if (gleft == 0) {
+          uint32_t g = kNone;
+          if (lane == 0) {
+            const uint32_t tp = atomicAdd(p.pool_ctr + band_idx, kGrab);
+            if (tp < p.pool_dbl) g = (uint32_t)p.pool_beg + tp * 64;
+          }
+          g = __shfl_sync(0xffffffffu, g, 0);
+          if (g == kNone) return kNone;
+          gbase = g;
+          gleft = kGrab;
         }
-        return __shfl_sync(0xffffffffu, g, 0);
+        const uint32_t r = gbase;
+        gbase += 64;
+        --gleft;
+        return r;
       };
-      uint32_t g = grab_pool();
-      if (g != kNone) {
-        issue_dbl(g, a0, a1);
-        issue_dbl(g + 64, b0i, b1i);
+      uint32_t ga = grab_pool(), gb = kNone;
+      if (ga != kNone) {
+        issue_dbl(ga, a0, a1);
+        gb = grab_pool();
+        if (gb != kNone) issue_dbl(gb, b0i, b1i);
       }
-      while (g != kNone) {
+      while (ga != kNone) {
         vote_full(a0);
         vote_full(a1);
-        issue_dbl(g + 128, a0, a1);
+        ga = gb == kNone ? kNone : grab_pool();
+        if (ga != kNone) issue_dbl(ga, a0, a1);
+        if (gb == kNone) break;
         vote_full(b0i);
         vote_full(b1i);
-        issue_dbl(g + 192, b0i, b1i);
-        vote_full(a0);
-        vote_full(a1);
-        g = grab_pool();
-        if (g != kNone) issue_dbl(g, a0, a1);
-        vote_full(b0i);
-        vote_full(b1i);
-        if (g != kNone) issue_dbl(g + 64, b0i, b1i);
+        gb = ga == kNone ? kNone : grab_pool();
+        if (gb != kNone) issue_dbl(gb, b0i, b1i);
       }
     }
   }
