@@ -569,6 +569,7 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
     p.edge_per_cta = (p.edge_items + per - 1) / per;
   }
   jp.nbands = n_bands;
+  jp.njobs = m;
   fn<<<dim3((unsigned)per, (unsigned)units), tfg::kThreads, smem, s>>>(jp);
   ck(cudaGetLastError(), "glcm_vote_jobs_kernel launch");
   ctx->launches++;

@@ -1101,7 +1101,7 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
 }
 
 // Several (d, theta) GLCMs of one image (or band batch) in ONE launch: grid
-// row y = job * nbands + band, x = the job's CTAs. Each job keeps its own
+// row y = band * njobs + job, x = the job's CTAs. Each job keeps its own
 // geometry; the reference-window variant (KSEL) is picked per CTA, so all
 // of an image's angles share one launch and its fixed costs (SURVEY.md §7
 // "small images are latency-bound"). Layouts without per-CTA partials
@@ -1111,12 +1111,15 @@ struct VoteJobs {
   VoteParams job[kMaxJobs];
   int ksel[kMaxJobs];
   int nbands;
+  int njobs;
 };
 
 template <int QUANT, int STRAT>
 __global__ void __launch_bounds__(kThreads, 1) glcm_vote_jobs_kernel(const __grid_constant__ VoteJobs jp) {
-  const int j = (int)blockIdx.y / jp.nbands;
-  const int band = (int)blockIdx.y - j * jp.nbands;
+  // band-major: the jobs of one band run side by side (adjacent blocks, the
+  // same wave), so a band is read from DRAM once and from L2 by the other jobs
+  const int band = (int)blockIdx.y / jp.njobs;
+  const int j = (int)blockIdx.y - band * jp.njobs;
   const VoteParams& p = jp.job[j];
   switch (jp.ksel[j]) {
     case 0: vote_cta<QUANT, STRAT, 0>(p, blockIdx.x, band); break;

@@ -31,12 +31,15 @@ enum Mode {
   M_HASH_128KB_RET,         // same, returning (the PACKED16 drain check)
   M_HASH_8WAY_INC,          // COPIES8 layout, hashed cells (L=64 on noise)
   M_HASH_16WAY_RET,         // 16 copies of packed u16 pairs, hashed cells, returning
+  M_HASH_16WAY_INC,         // same, non-returning (the L=64 16-copy layout's atomic ceiling)
+  M_HASH_16WAY_PAIRBANK,    // 16 copies, each owning 2 banks (lanes l, l+16), hashed cells, non-returning
   M_NMODES
 };
 const char* kNames[] = {"lane_private_inc", "lane_private_addn", "random_128KB_inc", "random_128KB_ret",
                         "random_16KB_inc", "same_addr_inc", "same_addr_addn", "lds_sts_private",
                         "copies8_random", "copies8_random_ret", "packed16x16_random_ret",
-                        "hashed_128KB_inc", "hashed_128KB_ret", "hashed_copies8_inc", "hashed_packed16x16_ret"};
+                        "hashed_128KB_inc", "hashed_128KB_ret", "hashed_copies8_inc", "hashed_packed16x16_ret",
+                        "hashed_packed16x16_inc", "hashed_16copies_2banks_inc"};
 
 __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
   h ^= h >> 16;
@@ -85,6 +88,16 @@ __global__ void __launch_bounds__(kT, 1) bench(unsigned long long* cycles, uint3
         break;
       }
       case M_HASH_8WAY_INC: atomicAdd(&s[((fmix32(h) & 4095) << 3) | (lane & 7)], 1u); break;
+      case M_HASH_16WAY_INC: {
+        const uint32_t x = fmix32(h);
+        atomicAdd(&s[((x & 2047) << 4) | (lane & 15)], 1u << ((x >> 11) & 16));
+        break;
+      }
+      case M_HASH_16WAY_PAIRBANK: {  // word (row, bank 2k + bit): lanes l, l+16 share banks 2k, 2k+1
+        const uint32_t x = fmix32(h);
+        atomicAdd(&s[((x & 1023) << 5) | ((lane & 15) << 1) | ((x >> 10) & 1)], 1u << ((x >> 11) & 16));
+        break;
+      }
       case M_HASH_16WAY_RET: {
         const uint32_t x = fmix32(h);
         acc |= atomicAdd(&s[((x & 2047) << 4) | (lane & 15)], 1u << ((x >> 11) & 16));
@@ -153,7 +166,7 @@ int main() {
   cudaMalloc(&sink, 64);
   using K = void (*)(unsigned long long*, uint32_t*);
   K ks[M_NMODES] = {bench<0>, bench<1>, bench<2>, bench<3>, bench<4>, bench<5>, bench<6>, bench<7>,
-                    bench<8>, bench<9>, bench<10>, bench<11>, bench<12>, bench<13>, bench<14>};
+                    bench<8>, bench<9>, bench<10>, bench<11>, bench<12>, bench<13>, bench<14>, bench<15>, bench<16>};
   for (auto k : ks) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
