@@ -776,9 +776,17 @@ def run_engine(args, wl):
         # results land by DMA in a pinned output buffer, one slice per call
         out_host = torch.zeros(o, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
 
+        multi_level = plan.layout != "bands" and len(plan.levels_list) > 1
+        e2e_jobs = [(L, d, a) for L in plan.levels_list for (d, a) in plan.dts]
+
         def e2e_step():
             off = 0
-            for L in plan.levels_list:
+            if multi_level:
+                # every (L, d, theta) of the step from ONE upload of each input
+                # (tfg_glcm_shard_jobs)
+                eng.shard_jobs(pinned["all"].numpy(), W, rows_e2e, plan.owned, e2e_jobs, n_bands=len(kinds),
+                               band_stride=rows_e2e * W, out=out_host)
+            for L in (() if multi_level else plan.levels_list):
                 dts = plan.dts
                 if plan.layout == "bands":
                     for kind in kinds:
@@ -825,11 +833,14 @@ def run_engine(args, wl):
             tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
             D.all_reduce_max_(tt)
             e2e_s = float(tt.item())
-        h2d = sum(v.numel() for v in pinned.values()) * len(plan.levels_list)
+        h2d = sum(v.numel() for v in pinned.values()) * (1 if multi_level else len(plan.levels_list))
         e2e = {"value": pairs_per_step / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": world * h2d,
                "d2h_bytes_per_step": world * o * 8,
-               "api": "tfg_glcm_shard / tfg_glcm_bands: every input of the step in one pinned host buffer, one "
-                      "call = one continuous Scheme-3 copy/vote stream pipeline, counts to host" + (", + NCCL reduce" if dist else ""),
+               "api": ("tfg_glcm_shard_jobs: every input of the step in one pinned host buffer, uploaded once for "
+                       "all its (L, d, theta)" if multi_level else
+                       "tfg_glcm_shard / tfg_glcm_bands: every input of the step in one pinned host buffer") +
+                      ", one call = one continuous Scheme-3 copy/vote stream pipeline, counts to host" +
+                      (", + NCCL reduce" if dist else ""),
                "pinned_h2d_GBps": max(h2d_gbs), "ms_per_step": e2e_s * 1e3,
                "h2d_bound_ms_per_step": h2d / (max(h2d_gbs) * 1e9) * 1e3}
 

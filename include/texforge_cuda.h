@@ -178,6 +178,18 @@ int tfg_glcm_shard(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t buffer_
                    const int* distances, const int* angles_deg, int n_dt, unsigned flags, uint64_t* counts_out);
 
 /*
+ * tfg_glcm_shard with per-job levels: job t = (levels[t], distances[t],
+ * angles_deg[t]); every band of the HOST image is copied up once and all its
+ * jobs vote from that copy (jobs that share a kernel instantiation in one
+ * launch). counts_out: [band][job][levels[t]^2] u64, jobs back to back.
+ * Counts only (no post-processing flags). n_jobs <= 64.
+ */
+int tfg_glcm_shard_jobs(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t buffer_rows, size_t owned_rows,
+                        size_t band_stride, size_t n_bands, int pixel_levels, const int* levels,
+                        const int* distances, const int* angles_deg, int n_jobs, unsigned flags,
+                        uint64_t* counts_out);
+
+/*
  * Scheme 3 (compute_glcm_chunked, pipeline.hpp:246-337): K row chunks from
  * partition(), fetched by `fetch` into a pinned ring, H2D on a copy stream
  * overlapped with voting on the exec stream into one device accumulator.

@@ -71,6 +71,8 @@ SIGNATURES = [
                                  _ip, C.c_int, C.c_uint, _u64p, _dp, _dp]),
     ("tfg_glcm_shard", C.c_int, [C.c_void_p, C.c_void_p, _sz, _sz, _sz, _sz, _sz, _sz, C.c_int, C.c_int, _ip, _ip,
                                  C.c_int, C.c_uint, _u64p]),
+    ("tfg_glcm_shard_jobs", C.c_int, [C.c_void_p, C.c_void_p, _sz, _sz, _sz, _sz, _sz, C.c_int, _ip, _ip, _ip, C.c_int,
+                                      C.c_uint, _u64p]),
     ("tfg_glcm_chunked", C.c_int, [C.c_void_p, _sz, _sz, C.c_int, C.c_int, _ip, _ip, C.c_int, _sz, FETCH_FN,
                                    C.c_void_p, C.c_uint, _u64p, _dp, _dp]),
     ("tfg_subglcms", C.c_int, [C.c_void_p, C.c_void_p, _sz, _sz, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint,

@@ -559,8 +559,12 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
   // one wave of CTAs split evenly over the (job, band) units (launch_vote's rule per unit)
   const long long units = (long long)m * n_bands;
   const long long slots = (long long)ctx->num_sms * bps;
+  static const long long waves = [] {
+    const char* e = std::getenv("TEXFORGE_JOBS_WAVES");  // A/B knob: CTA waves when units exceed the SM slots
+    return e ? std::max(1ll, std::atoll(e)) : 8ll;
+  }();
   long long per = units < slots ? std::max<long long>(1, slots / units)
-                                : std::max<long long>(1, (8 * slots + units - 1) / units);
+                                : std::max<long long>(1, (waves * slots + units - 1) / units);
   per = std::max<long long>(1, std::min<long long>(per, (max_items + 2 * tfg::kThreads - 1) / (2 * tfg::kThreads)));
   if (units > 65535) return false;
   for (int j = 0; j < m; ++j) {
@@ -693,6 +697,27 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
                                                             n_bands, d_glcm);
     ck(cudaGetLastError(), "glcm_reduce_partials_kernel launch");
     ctx->launches++;
+  }
+}
+
+// Enqueues jobs with per-job (L, d, theta), job t adding into outs[t] (band b
+// at + b * L_t^2): runs that share a kernel instantiation go out as one
+// multi-job launch of up to kMaxJobs, the rest one launch per job (all
+// ordered on `s`).
+void launch_job_set(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
+                    size_t band_stride, int n_bands, size_t row_end, int pixel_levels, const int* levels,
+                    const int* distances, const int* angles, unsigned long long* const* outs, int n_jobs,
+                    unsigned flags, cudaStream_t s) {
+  int t = 0;
+  while (t < n_jobs) {
+    int n = std::min(n_jobs - t, tfg::kMaxJobs);
+    while (n > 1 && !launch_vote_jobs(ctx, d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels,
+                                       levels + t, distances + t, angles + t, outs + t, n, flags, s))
+      --n;
+    if (n == 1)
+      launch_vote(ctx, d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels, levels[t],
+                  distances[t], angles[t], flags, outs[t], s);
+    t += n;
   }
 }
 
@@ -877,7 +902,10 @@ template <typename Fetch>
 void run_pipeline_specs(tfg_ctx* ctx, size_t width, const std::vector<uint64_t>& specs, int pixel_levels,
                         int levels, const int* distances, const int* angles, int n_dt, unsigned flags,
                         unsigned long long* d_acc, Fetch&& fetch_rows, size_t n_bands = 1,
-                        size_t acc_band_stride = 0, const std::function<void(size_t)>& band_done = nullptr) {
+                        size_t acc_band_stride = 0, const std::function<void(size_t)>& band_done = nullptr,
+                        const int* job_levels = nullptr, const size_t* job_off = nullptr) {
+  // job_levels / job_off: per-job L and offset inside a band's slice of d_acc
+  // (tfg_glcm_shard_jobs); null = every job at `levels`, job t at t * L^2
   // The ring runs continuously over (band, chunk): band b+1's first copy
   // overlaps band b's last votes. Band b's GLCMs go to d_acc + b*acc_band_stride.
   const size_t k = specs.size() / 3;
@@ -901,11 +929,18 @@ void run_pipeline_specs(tfg_ctx* ctx, size_t width, const std::vector<uint64_t>&
     ck(cudaEventRecord(ctx->copied[sl], ctx->copy), "event record");
     ck(cudaStreamWaitEvent(ctx->exec, ctx->copied[sl], 0), "wait");
     if (pixel_levels == levels) launch_validate(ctx, dst, width, rows, pitch, 0, 1, levels, sync_err(ctx), ctx->exec);
-    if (!launch_vote_jobs(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, levels, distances,
-                          angles, n_dt, flags, d_acc + bnd * acc_band_stride, (size_t)levels * levels, ctx->exec))
+    if (job_levels) {
+      unsigned long long* outs[64];
+      for (int t = 0; t < n_dt; ++t) outs[t] = d_acc + bnd * acc_band_stride + job_off[t];
+      launch_job_set(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, job_levels, distances, angles,
+                     outs, n_dt, flags, ctx->exec);
+    } else if (!launch_vote_jobs(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, levels,
+                                 distances, angles, n_dt, flags, d_acc + bnd * acc_band_stride,
+                                 (size_t)levels * levels, ctx->exec)) {
       for (int t = 0; t < n_dt; ++t)
         launch_vote(ctx, dst, width, rows, pitch, 0, 1, owned_end - start, pixel_levels, levels, distances[t],
                     angles[t], flags, d_acc + bnd * acc_band_stride + (size_t)t * levels * levels, ctx->exec);
+    }
     ck(cudaEventRecord(ctx->consumed[sl], ctx->exec), "event record");
     if (band_done && i == k - 1) band_done(bnd);
     if (sequential) ck(cudaStreamSynchronize(ctx->exec), "stream sync");
@@ -916,10 +951,11 @@ template <typename Fetch>
 void run_pipeline(tfg_ctx* ctx, size_t width, size_t height, int pixel_levels, int levels,
                   const int* distances, const int* angles, int n_dt, size_t k, unsigned flags,
                   unsigned long long* d_acc, Fetch&& fetch_rows, size_t total_rows = 0, size_t n_bands = 1,
-                  size_t acc_band_stride = 0, const std::function<void(size_t)>& band_done = nullptr) {
+                  size_t acc_band_stride = 0, const std::function<void(size_t)>& band_done = nullptr,
+                  const int* job_levels = nullptr, const size_t* job_off = nullptr) {
   run_pipeline_specs(ctx, width, chunk_specs(width, height, distances, angles, n_dt, k, total_rows), pixel_levels,
                      levels, distances, angles, n_dt, flags, d_acc, std::forward<Fetch>(fetch_rows), n_bands,
-                     acc_band_stride, band_done);
+                     acc_band_stride, band_done, job_levels, job_off);
 }
 
 // Shared-memory budget of glcm_subglcm_kernel's R sub-GLCM copies.
@@ -960,7 +996,8 @@ void stage_host_image(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t heig
 void host_vote(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t owned_rows, size_t band_stride,
                size_t n_bands, int pixel_levels, int levels, const int* distances, const int* angles_deg, int n_dt,
                unsigned flags, unsigned long long* d_acc,
-               const std::function<void(size_t)>& band_done = nullptr) {
+               const std::function<void(size_t)>& band_done = nullptr, const int* job_levels = nullptr,
+               const size_t* job_off = nullptr, size_t job_band_words = 0) {
   int dmax = 1;
   for (int i = 0; i < n_dt; ++i) dmax = std::max(dmax, distances[i]);
   const size_t k = auto_chunks(width, owned_rows, dmax);
@@ -971,7 +1008,7 @@ void host_vote(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, siz
     for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, sp[3 * i + 2] - sp[3 * i]);
     for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->hslot[sl].get(max_rows * width + 64);
   }
-  const size_t band_words = (size_t)n_dt * levels * levels;
+  const size_t band_words = job_levels ? job_band_words : (size_t)n_dt * levels * levels;
   run_pipeline(
       ctx, width, owned_rows, pixel_levels, levels, distances, angles_deg, n_dt, k, flags, d_acc,
       [&](size_t b, size_t, size_t start, size_t, size_t buf_end, int sl) -> const uint8_t* {
@@ -981,7 +1018,7 @@ void host_vote(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, siz
         parallel_memcpy(dst, src, (buf_end - start) * width);
         return dst;
       },
-      height, n_bands, band_words, band_done);
+      height, n_bands, band_words, band_done, job_levels, job_off);
 }
 
 }  // namespace
@@ -1300,6 +1337,67 @@ int tfg_glcm_shard(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t buffer_
   return glcm_impl(ctx, px, width, buffer_rows, owned_rows, pitch, n_bands > 1 ? band_stride : pitch * buffer_rows,
                    n_bands, pixel_levels, levels, distances, angles_deg, n_dt,
                    flags & ~(TFG_SYMMETRIC | TFG_NORMALIZE | TFG_FEATURES), counts_out, nullptr, nullptr);
+}
+
+int tfg_glcm_shard_jobs(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t buffer_rows, size_t owned_rows,
+                        size_t band_stride, size_t n_bands, int pixel_levels, const int* levels,
+                        const int* distances, const int* angles_deg, int n_jobs, unsigned flags,
+                        uint64_t* counts_out) {
+  if (!ctx) { g_error = "null context"; return TFG_INVALID_ARGUMENT; }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded([&] {
+    if (n_jobs < 1 || n_jobs > 64 || !levels) fail(TFG_INVALID_ARGUMENT, "glcm: need 1..64 jobs");
+    for (int t = 0; t < n_jobs; ++t) {
+      check_levels(levels[t], "glcm");
+      check_pixel_levels(pixel_levels, levels[t]);
+    }
+    if (width == 0 || buffer_rows == 0) fail(TFG_INVALID_ARGUMENT, "QuantizedImage: dimensions must be positive");
+    if (flags & TFG_INPUT_DEVICE)
+      fail(TFG_INVALID_ARGUMENT, "glcm_shard_jobs: host images only (device images: tfg_glcm_jobs_async)");
+    if (n_bands < 1) fail(TFG_INVALID_ARGUMENT, "glcm: need at least one band");
+    if (n_bands > 1 && band_stride < width * buffer_rows) fail(TFG_INVALID_ARGUMENT, "glcm: bands overlap");
+    check_dts(distances, angles_deg, n_jobs, width, buffer_rows);
+    if (!px) fail(TFG_INVALID_ARGUMENT, "glcm: null pixels");
+    if (owned_rows > buffer_rows) fail(TFG_INVALID_ARGUMENT, "glcm: owned rows exceed the buffer rows");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = ctx->exec;
+    std::vector<size_t> off((size_t)n_jobs);
+    size_t band_words = 0;
+    for (int t = 0; t < n_jobs; ++t) {
+      off[t] = band_words;
+      band_words += (size_t)levels[t] * levels[t];
+    }
+    const size_t words = n_bands * band_words;
+    auto* d_acc = static_cast<unsigned long long*>(ctx->acc.get(words * 8));
+    ck(cudaMemsetAsync(d_acc, 0, words * 8, s), "memset");
+    if (owned_rows > 0) {
+      if (pixel_levels < 256) clear_sync_flag(ctx, s);
+      const bool early = n_bands > 1 && counts_out && host_memory_kind(counts_out) == 1;
+      auto band_done = [&](size_t b) {
+        if (b + 1 >= n_bands) return;
+        ck(cudaEventRecord(ctx->band_ev, ctx->exec), "event record");
+        ck(cudaStreamWaitEvent(ctx->aux[0], ctx->band_ev, 0), "wait");
+        ck(cudaMemcpyAsync(counts_out + b * band_words, d_acc + b * band_words, band_words * 8,
+                           cudaMemcpyDeviceToHost, ctx->aux[0]),
+           "D2H band counts");
+      };
+      struct AuxDrain {
+        cudaStream_t st;
+        bool on;
+        ~AuxDrain() {
+          if (on) cudaStreamSynchronize(st);
+        }
+      } drain{ctx->aux[0], early};
+      host_vote(ctx, px, width, buffer_rows, owned_rows, n_bands > 1 ? band_stride : width * buffer_rows, n_bands,
+                pixel_levels, levels[0], distances, angles_deg, n_jobs, flags & ~(TFG_SYMMETRIC | TFG_NORMALIZE | TFG_FEATURES),
+                d_acc, early ? std::function<void(size_t)>(band_done) : nullptr, levels, off.data(), band_words);
+      if (pixel_levels < 256) check_sync_flag(ctx, s);
+      // counts only: one u64 "cell" per word
+      finish(ctx, d_acc, (int)words, 1, 0, counts_out, nullptr, nullptr, s, early ? (n_bands - 1) * band_words : 0);
+    } else {
+      finish(ctx, d_acc, (int)words, 1, 0, counts_out, nullptr, nullptr, s);
+    }
+  });
 }
 
 int tfg_glcm(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t height, size_t pitch, int pixel_levels,
@@ -1690,20 +1788,8 @@ int tfg_glcm_jobs_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t 
       outs[t] = reinterpret_cast<unsigned long long*>(d_counts) + off;
       off += n_bands * (size_t)levels[t] * levels[t];
     }
-    // runs of jobs that share a kernel instantiation go out as one launch of
-    // up to kMaxJobs; the rest one launch per job (ordered on `s`)
-    int t = 0;
-    while (t < n_jobs) {
-      int n = std::min(n_jobs - t, tfg::kMaxJobs);
-      while (n > 1 && !launch_vote_jobs(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, row_end,
-                                         pixel_levels, levels + t, distances + t, angles_deg + t, outs.data() + t, n,
-                                         flags, s))
-        --n;
-      if (n == 1)
-        launch_vote(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, row_end, pixel_levels, levels[t],
-                    distances[t], angles_deg[t], flags, outs[t], s);
-      t += n;
-    }
+    launch_job_set(ctx, d_px, width, height, pitch, band_stride, (int)n_bands, row_end, pixel_levels, levels,
+                   distances, angles_deg, outs.data(), n_jobs, flags, s);
   });
 }
 

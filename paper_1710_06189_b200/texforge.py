@@ -367,6 +367,33 @@ class Engine:
                                          pixel_levels, levels, d, a, n_dt, flags, _ptr(counts, C.c_uint64)))
         return counts.reshape(n_bands, n_dt, levels, levels)
 
+    def shard_jobs(self, pixels: np.ndarray, width: int, buffer_rows: int, owned_rows: int,
+                   jobs: Sequence[Tuple[int, int, int]], pixel_levels: int = 256, n_bands: int = 1,
+                   band_stride: int = 0, out: Optional[np.ndarray] = None) -> list:
+        """tfg_glcm_shard_jobs: per-job (L, d, theta) counts of a HOST row shard /
+        band batch, each band copied up once for all its jobs. Returns, per
+        job, counts[n_bands, L, L] (views into one [band][job] buffer)."""
+        n = len(jobs)
+        lv = (C.c_int * n)(*[int(j[0]) for j in jobs])
+        d = (C.c_int * n)(*[int(j[1]) for j in jobs])
+        a = (C.c_int * n)(*[int(j[2]) for j in jobs])
+        band_words = sum(int(j[0]) ** 2 for j in jobs)
+        counts = _out_buffer(out, n_bands * band_words)
+        stride = band_stride or width * buffer_rows
+        px = np.ascontiguousarray(pixels, dtype=np.uint8).reshape(-1)
+        if px.size < stride * (n_bands - 1) + width * buffer_rows:
+            raise ValueError("glcm: pixel count does not match dimensions")
+        L.check(self._lib.tfg_glcm_shard_jobs(self.handle, px.ctypes.data_as(C.c_void_p), width, buffer_rows,
+                                              owned_rows, stride, n_bands, pixel_levels, lv, d, a, n, 0,
+                                              _ptr(counts, C.c_uint64)))
+        per_band = counts.reshape(n_bands, band_words)
+        res, off = [], 0
+        for j in jobs:
+            c = int(j[0]) ** 2
+            res.append(per_band[:, off:off + c].reshape(n_bands, int(j[0]), int(j[0])))
+            off += c
+        return res
+
     def chunked(self, source: ChunkSource, dts: Sequence[Tuple[int, int]], chunk_count: int,
                 pixel_levels: int, levels: int, flags: int = 0) -> np.ndarray:
         width, height = source.width(), source.height()

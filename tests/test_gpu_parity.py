@@ -558,3 +558,22 @@ def test_jobs_async_mixed_levels(engine, nb):
             want = O.glcm_gray(imgs[b], w, h, levels, d, a)
             assert np.array_equal(got[off + b * cells: off + (b + 1) * cells], want), (levels, d, a, b)
         off += nb * cells
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_shard_jobs_one_upload_many_levels(engine, pinned):
+    # tfg_glcm_shard_jobs: host bands copied up once; every (L, d, theta) job
+    # votes from that copy; owned rows + halo like tfg_glcm_shard
+    import torch
+    w, rows, owned, nb = 1500, 700, 690, 2
+    imgs = [tf.synth_noise(w, rows, 71).pixels, tf.synth_smooth(w, rows, 72).pixels]
+    host = np.concatenate(imgs)
+    if pinned:
+        t = torch.from_numpy(host).pin_memory()
+        host = t.numpy()
+    jobs = [(16, 1, 0), (16, 1, 45), (32, 1, 90), (32, 2, 135), (64, 1, 0), (256, 3, 45), (8, 4, 90)]
+    got = engine.shard_jobs(host, w, rows, owned, jobs, n_bands=nb)
+    for t, (levels, d, a) in enumerate(jobs):
+        for b in range(nb):
+            want = _oracle_rows(imgs[b], w, rows, levels, d, a, owned)
+            assert np.array_equal(got[t][b].reshape(-1), want), (levels, d, a, b)
