@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-2 evidence pass (run under gpurun). Outputs in gpurun_out/r02e/ (profiles/README.md).
-O=gpurun_out/r02e; mkdir -p $O
+O=${R02_OUT:-gpurun_out/r02e}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,power.limit --format=csv > $O/info.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
@@ -30,3 +30,8 @@ for L in 8 32 256; do for K in noise smooth; do
 done; done
 for L in 256 128 64 32 16 8; do timeout 300 python tools/profile_vote.py --levels $L --dts 1:0,1:45,2:90,4:135 --reps 5 --time > $O/kernel_L$L.json 2>&1; done
 bash tools/sanitize.sh > /dev/null 2>&1; cp -r gpurun_out/sanitizer $O/ 2>/dev/null
+# per-workload DRAM traffic of one bench step (roofline.traffic)
+for wl in c2 c4 c5 c1; do
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:glcm --csv --log-file $O/launches_$wl.csv python bench.py --workload $wl --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $O/traffic_$wl.log 2>&1
+done
+timeout 600 ./tools/atomics_bench > $O/atomics.json 2>&1
