@@ -68,7 +68,8 @@ enum tfg_strategy {
   TFG_STRAT_COPIES32 = 1, /* 32 lane-interleaved u32 sub-GLCM copies per CTA (L <= 32)  */
   TFG_STRAT_COPIES8 = 2,  /* 8 interleaved u32 copies per CTA (L <= 64)                 */
   TFG_STRAT_COPY1 = 3,    /* one u32 copy per CTA (L <= 238)                            */
-  TFG_STRAT_PACKED16 = 4  /* one copy of packed u16 counters + exact spill (L <= 256)   */
+  TFG_STRAT_PACKED16 = 4, /* one copy of packed u16 counters + exact spill (L <= 256)   */
+  TFG_STRAT_P16X16 = 5    /* 16 bank-pair copies of packed u16 counters (L <= 64)       */
 };
 
 typedef struct tfg_ctx tfg_ctx;

@@ -28,7 +28,7 @@ TFG_SCHEME_GLOBAL = 1 << 4
 TFG_SEQUENTIAL = 1 << 5
 
 TFG_STRATEGY_SHIFT = 16
-STRAT_AUTO, STRAT_COPIES32, STRAT_COPIES8, STRAT_COPY1, STRAT_PACKED16 = range(5)
+STRAT_AUTO, STRAT_COPIES32, STRAT_COPIES8, STRAT_COPY1, STRAT_PACKED16, STRAT_P16X16 = range(6)
 
 
 def strategy_flag(s: int) -> int:

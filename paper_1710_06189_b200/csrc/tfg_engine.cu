@@ -192,7 +192,8 @@ int pick_strategy(int levels, unsigned flags) {
   const int forced = (int)((flags >> TFG_STRATEGY_SHIFT) & 0xF);
   if (forced) {
     const bool ok = (forced == TFG_STRAT_COPIES32 && levels <= 32) || (forced == TFG_STRAT_COPIES8 && levels <= 64) ||
-                    (forced == TFG_STRAT_COPY1 && levels <= 128) || (forced == TFG_STRAT_PACKED16);
+                    (forced == TFG_STRAT_COPY1 && levels <= 128) || (forced == TFG_STRAT_PACKED16) ||
+                    (forced == TFG_STRAT_P16X16 && levels <= 64);
     if (!ok) fail(TFG_INVALID_ARGUMENT, "strategy does not support these levels");
     return forced;
   }
@@ -210,6 +211,7 @@ size_t hist_words_of(int strat, int levels) {
     case tfg::S_COPIES32: w = L * 32 * 32; break;   // cells a + 32b, 32 copies
     case tfg::S_COPIES8: w = L * 64 * 8; break;     // cells b + 64a, 8 copies
     case tfg::S_COPY1: w = L * 128; break;          // cells a + 128b
+    case tfg::S_P16X16: w = 32768; break;           // 16 copies x 2048 words (c = 64b + a)
     default: w = std::min<size_t>(L * 256, 32768); break;  // words (a + 256b) & 0x7fff
   }
   return (w + 3) & ~size_t(3);

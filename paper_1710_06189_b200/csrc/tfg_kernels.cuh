@@ -55,6 +55,7 @@ enum Strat : int {
   S_COPIES32 = 1,  // L <= 32:  32 u32 copies [a + 32b][lane]; P = 8a, Q = b, addr = 16x + 4 lane
   S_COPIES8 = 2,   // L <= 64:  8 u32 copies [b + 64a][lane%8]; P = 4b, Q = a, addr = 8x + 4 (lane%8)
   S_COPY1 = 3,     // L <= 128: 1 u32 copy [a + 128b]; P = 2a, Q = b, addr = 2x
+  S_P16X16 = 5,    // L <= 64: 16 copies of u16 counters, copy = lane & 15 owning banks 2k, 2k+1 (p16x16_*)
   S_PACKED16 = 4   // L <= 256: 1 copy of u16 counters, cell a + 256b in word (x & 0x7fff), half b >> 7,
                    //           drained to the u64 cells past 2^15 (kDrainBit)
 };
@@ -277,6 +278,86 @@ __device__ __forceinline__ void packed_vote16(uint32_t hb, const uint32_t (&P)[4
     for (int j = 0; j < 4; ++j) flag |= atom_smem(hb + pair_x(P[i], Qm, j) * 4u, packed_inc(Q[i], j));
   }
   if (flag & kDrainBit) packed_drain_item(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], 0xFFFFu, glcm, L);
+}
+
+// ---- S_P16X16 (L <= 64): 16 copies of packed u16 counters. Lanes l and
+// l+16 share copy k = l & 15, which owns banks 2k and 2k+1, so an ATOMS costs
+// ~2 wavefronts instead of COPIES8's 2.93 (random cells, 4 lanes per 4-bank
+// group). Cell (ref b, anchor a): half = a & 1; copy k's word
+// A1(a) + 256 b + 16384 (a >> 5) + 2k, with A1 = bits {(a>>1)&1 -> 0,
+// (a>>2)&7 -> 5..7}: bank = ((a >> 1) & 1) + 2k, so the two lanes of a copy
+// share its two banks and no other copy touches them. Per 4-pixel anchor
+// word: A1, A2 = (a >> 5) & 1, Ah = (a & 1) << 7. A vote: x = PRMT(A1, B) =
+// A1_j + 256 b_j; y = PRMT(A2, hb) = hb with byte 2 := a>>5 (+65536 bytes,
+// the address bit a byte cannot hold next to the 4 lane bits); address =
+// 4x + y; increment 1 or 0x10000 from Ah's sign; overflow exactly as
+// PACKED16 (kDrainBit). Measured: 2.02 wavefronts per ATOMS (COPIES8 2.93),
+// but ~2x the instructions per vote (issue-bound) and no POPC.INC
+// aggregation for smooth input: slower than COPIES8.
+struct P16x16Words {
+  uint32_t A1[4], A2[4], Ah[4], B[4];
+};
+__device__ __forceinline__ void p16x16_prep(const uint32_t (&qa)[4], const uint32_t (&qb)[4], P16x16Words& w) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    w.A1[i] = ((qa[i] >> 1) & 0x01010101u) | ((qa[i] << 3) & 0xE0E0E0E0u);
+    w.A2[i] = (qa[i] >> 5) & 0x01010101u;
+    w.Ah[i] = (qa[i] << 7) & 0x80808080u;
+    w.B[i] = qb[i];
+  }
+}
+__device__ __forceinline__ uint32_t p16x16_addr(uint32_t hb, const P16x16Words& w, int i, int j) {
+  const uint32_t x = pair_x(w.A1[i], w.B[i], j);
+  const uint32_t y = prmt(w.A2[i], hb, 0x7004u | ((uint32_t)j << 8) | 0x50u);
+  return x * 4u + y;
+}
+// drains word `addr` holding cells (b, a & ~1) [low half] and (b, a | 1) [high half]
+__device__ __forceinline__ void p16x16_drain(uint32_t addr, uint32_t a, uint32_t b, unsigned long long* glcm,
+                                             uint32_t L) {
+  uint32_t old;
+  asm volatile("atom.shared.and.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(0x07FF07FFu) : "memory");
+  const uint32_t lo = old & 0xF800u, hi = (old >> 16) & 0xF800u;
+  if (lo) atomicAdd(glcm + b * L + (a & ~1u), (unsigned long long)lo);
+  if (hi) atomicAdd(glcm + b * L + (a | 1u), (unsigned long long)hi);
+}
+static __device__ __noinline__ void p16x16_drain_item(uint32_t hb, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                                      uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3,
+                                                      uint32_t mask, unsigned long long* glcm, uint32_t L) {
+  const uint32_t a4[4] = {a0, a1, a2, a3}, b4[4] = {b0, b1, b2, b3};
+  const uint32_t* qa = a4;
+  const uint32_t* qb = b4;
+  P16x16Words w;
+  p16x16_prep(a4, b4, w);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (mask & (1u << k)) {
+      const int i = k >> 2, j = k & 3;
+      p16x16_drain(p16x16_addr(hb, w, i, j), (qa[i] >> (8 * j)) & 0xFFu, (qb[i] >> (8 * j)) & 0xFFu, glcm, L);
+    }
+  }
+}
+// the pairs in `mask` of one item (qa: quantised anchors, qb: quantised references)
+__device__ __forceinline__ void p16x16_vote(uint32_t hb, const uint32_t (&qa)[4], const uint32_t (&qb)[4],
+                                            uint32_t mask, unsigned long long* glcm, uint32_t L) {
+  P16x16Words w;
+  p16x16_prep(qa, qb, w);
+  uint32_t flag = 0;
+  if (mask == 0xFFFFu) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        flag |= atom_smem(p16x16_addr(hb, w, i, j), prmt(w.Ah[i], 0u, 0x4400u | ((8u + j) << 4) | (8u + j)) + 1u);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int i = k >> 2, j = k & 3;
+      if (mask & (1u << k))
+        flag |= atom_smem(p16x16_addr(hb, w, i, j), prmt(w.Ah[i], 0u, 0x4400u | ((8u + j) << 4) | (8u + j)) + 1u);
+    }
+  }
+  if (flag & kDrainBit)
+    p16x16_drain_item(hb, qa[0], qa[1], qa[2], qa[3], qb[0], qb[1], qb[2], qb[3], mask, glcm, L);
 }
 
 // Votes the 16 pixel pairs of one item. Returns true when the run-length
@@ -660,6 +741,7 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
   uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(hist));
   if constexpr (STRAT == S_COPIES32) hb += lane * 4u;
   if constexpr (STRAT == S_COPIES8) hb += (lane & 7u) * 4u;
+  if constexpr (STRAT == S_P16X16) hb += (lane & 15u) * 8u;  // byte 2 of hb stays 0 (p16x16_addr)
 
   const uint32_t pitch = (uint32_t)p.pitch;
   const uint32_t nch = (uint32_t)p.nch;
@@ -668,7 +750,22 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
   bool rle = true;  // PACKED16 run-length check; re-sampled every 8th item when it stops paying
   uint32_t nb = 0;
   // Votes one item (16 pairs, or the pairs in `mask`).
+  // S_P16X16: quantised anchor / reference words of an item
+  auto p16x16_item = [&](const RawItem& cur, uint32_t mask) {
+    uint32_t A[4], R[4], qa[4], qb[4];
+    ref_words<KSEL>(p, cur, A, R);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      qa[i] = quant4<QUANT>(A[i], p);
+      qb[i] = quant4<QUANT>(R[i], p);
+    }
+    p16x16_vote(hb, qa, qb, mask, glcm, L);
+  };
   auto vote_item = [&](const RawItem& cur) {
+    if constexpr (STRAT == S_P16X16) {
+      if (cur.mask) p16x16_item(cur, cur.mask);
+      return;
+    }
     uint32_t P[4], Q[4];
     item_words<QUANT, STRAT, KSEL>(p, cur, P, Q);
     if constexpr (STRAT == S_PACKED16) {
@@ -689,6 +786,10 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
 
   // An unmasked item of the main pass (all 16 pairs vote).
   auto vote_full = [&](const RawItem& cur) {
+    if constexpr (STRAT == S_P16X16) {
+      p16x16_item(cur, 0xFFFFu);
+      return;
+    }
     uint32_t P[4], Q[4];
     item_words<QUANT, STRAT, KSEL>(p, cur, P, Q);
     if constexpr (STRAT == S_PACKED16) {
@@ -1081,6 +1182,19 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
             for (unsigned int b = 0; b < gridDim.y; ++b) reinterpret_cast<volatile unsigned int*>(p.pool_ctr)[b] = 0u;
         }
       }
+    }
+    return;
+  }
+  if constexpr (STRAT == S_P16X16) {
+    // cell (b, a): copy k's field at word A1(a) + 256 b + 16384 (a >> 5) + 2k, half a & 1 (p16x16_addr)
+    for (int cc = tid; cc < cells; cc += kThreads) {
+      const uint32_t b = (uint32_t)cc / L, a = (uint32_t)cc - b * L;
+      const uint32_t a1 = ((a >> 1) & 1u) | (((a >> 2) & 7u) << 5);
+      const uint32_t base = a1 + 256u * b + 16384u * (a >> 5), sh = 16u * (a & 1u);
+      uint32_t sum = 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) sum += (hist[base + 2u * ((k + lane) & 15u)] >> sh) & 0xFFFFu;
+      if (sum) atomicAdd(glcm + cc, (unsigned long long)sum);
     }
     return;
   }

@@ -36,6 +36,7 @@ VoteKernel TFG_CAT(tfg_pick_vote_q, TFG_QUANT)(int strat, int ksel) {
     case tfg::S_COPIES32: return pick_k<Q, tfg::S_COPIES32>(ksel);
     case tfg::S_COPIES8: return pick_k<Q, tfg::S_COPIES8>(ksel);
     case tfg::S_COPY1: return pick_k<Q, tfg::S_COPY1>(ksel);
+    case tfg::S_P16X16: return pick_k<Q, tfg::S_P16X16>(ksel);
     default: return pick_k<Q, tfg::S_PACKED16>(ksel);
   }
 }
@@ -47,6 +48,7 @@ JobsKernel TFG_CAT(tfg_pick_jobs_q, TFG_QUANT)(int strat) {
   switch (strat) {
     case tfg::S_COPIES32: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_COPIES32>;
     case tfg::S_COPIES8: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_COPIES8>;
+    case tfg::S_P16X16: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_P16X16>;
     default: return nullptr;
   }
 }

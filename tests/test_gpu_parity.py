@@ -22,6 +22,7 @@ def _strategies_for(levels):
         s.append(L.STRAT_COPY1)
     if levels <= 64:
         s.append(L.STRAT_COPIES8)
+        s.append(L.STRAT_P16X16)
     if levels <= 32:
         s.append(L.STRAT_COPIES32)
     return s
@@ -577,3 +578,21 @@ def test_shard_jobs_one_upload_many_levels(engine, pinned):
         for b in range(nb):
             want = _oracle_rows(imgs[b], w, rows, levels, d, a, owned)
             assert np.array_equal(got[t][b].reshape(-1), want), (levels, d, a, b)
+
+
+@pytest.mark.parametrize("pattern", ["constant", "alternating", "stripes"])
+def test_p16x16_drains_exact(engine, pattern):
+    # S_P16X16: 16 copies of u16 fields; > 2^15 votes per copy per CTA on
+    # single cells (8192 x 16384 at L=64: ~900K votes per CTA, ~57K per copy
+    # on a constant image: the drain path runs; forced strategy)
+    w, h = 8192, 16384
+    if pattern == "constant":
+        img = np.full(w * h, 200, np.uint8)
+    elif pattern == "alternating":
+        img = np.tile(np.array([10, 250], np.uint8), w * h // 2)
+    else:
+        row = np.where((np.arange(w) // 3) % 2 == 0, 7, 131).astype(np.uint8)
+        img = np.tile(row, h)
+    for d, a in [(1, 0), (1, 90), (2, 45), (3, 135)]:
+        got = engine.glcm(img, w, h, 64, [(d, a)], flags=L.strategy_flag(L.STRAT_P16X16))
+        assert np.array_equal(got.reshape(-1), O.glcm_gray(img, w, h, 64, d, a)), (pattern, d, a)
