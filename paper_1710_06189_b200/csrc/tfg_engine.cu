@@ -640,7 +640,16 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   // With partials and a grid that is co-resident (one CTA per SM slot), the
   // kernel reduces the partials itself behind a grid barrier (cooperative
   // launch guarantees co-residency); larger grids use the reduce kernels.
-  const bool in_kernel_reduce = use_partials && per_band * n_bands <= (long long)ctx->num_sms * bps;
+  // TEXFORGE_COOP=0: A/B knob for the L > 64 merge, split-K reduce kernels
+  // instead of the cooperative launch with the in-kernel reduce (measured:
+  // a cooperative launch costs the same as a plain one; the fixed cost of an
+  // L=256 launch is ~18 us in-kernel vs ~10 us split-K, but 135 vs 156 us at
+  // 16384^2: tools/launch_overhead.py)
+  static const int coop_mode = [] {
+    const char* e = std::getenv("TEXFORGE_COOP");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool in_kernel_reduce = coop_mode != 0 && use_partials && per_band * n_bands <= (long long)ctx->num_sms * bps;
   if (in_kernel_reduce && n_bands <= kMaxPoolBands &&
       (strat == tfg::S_PACKED16 || strat == tfg::S_COPY1)) {  // the layouts with the pool loop
     // The grid barrier waits for the slowest CTA, so the last pool_pct % of
