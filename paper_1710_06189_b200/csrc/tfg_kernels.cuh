@@ -822,6 +822,39 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
   const uint8_t* const abase0 = band + ((p.ch0 + p.js) << 4);
   const uint8_t* const rbase0 = abase0 + p.ref_off;
   // f0: first item of the double batch (warp-uniform)
+#ifndef TFG_NBR_SHFL
+#define TFG_NBR_SHFL 1
+#endif
+  // Reference windows with one narrow word (d <= 3 at 0 / 135 degrees: the
+  // next segment's first word; 45 degrees: the previous segment's last word):
+  // in a double batch that does not wrap a row, that word is the adjacent
+  // lane's anchor / reference segment, so it comes by one shuffle per item
+  // instead of a 4-byte load per lane (a strided LDG.32 touches the same 4-5
+  // L1 lines as a full LDG.128).
+  // Enabled for COPIES8 (L <= 64), whose kernel is bound by the L1 data pipe
+  // (noise L=64: -3..-6% per call); the issue-bound layouts (COPIES32 and
+  // PACKED16 on smooth input) lose more to the extra shuffles than they gain.
+  constexpr bool kNbrShfl = TFG_NBR_SHFL && STRAT == S_COPIES8 && (KSEL == 5 || KSEL == 0 || KSEL == 3);
+  constexpr uint32_t kNbrPending = 0x10000u;  // RawItem.mask of a main-pass x0 (vote_full ignores masks)
+  auto nbr_fix = [&](RawItem& x0, RawItem& x1) {
+    if constexpr (kNbrShfl) {
+      if (x0.mask != kNbrPending) return;  // warp-uniform: the row-wrap path loaded the words
+      const uint32_t nxt = (lane + 1) & 31u, prv = (lane + 31) & 31u;
+      if constexpr (KSEL == 3) {
+        const uint32_t p1 = lane == 31 ? x0.c1.w : x1.c1.w;
+        const uint32_t w0 = __shfl_sync(0xffffffffu, x0.c1.w, prv);
+        const uint32_t w1 = __shfl_sync(0xffffffffu, p1, prv);
+        if (lane != 0) x0.c0.w = w0;
+        x1.c0.w = w1;
+      } else {
+        const uint32_t v0 = KSEL == 5 ? x0.a.x : x0.c0.x, v1 = KSEL == 5 ? x1.a.x : x1.c0.x;
+        const uint32_t w0 = __shfl_sync(0xffffffffu, lane == 0 ? v1 : v0, nxt);
+        const uint32_t w1 = __shfl_sync(0xffffffffu, v1, nxt);
+        x0.c1.x = w0;
+        if (lane != 31) x1.c1.x = w1;
+      }
+    }
+  };
   auto issue_dbl = [&](uint32_t f0, RawItem& x0, RawItem& x1) {
     const uint32_t row0 = fast_div(f0, p.ni_mul, p.ni_shr);
     const uint32_t jj0 = f0 - row0 * ni;
@@ -835,6 +868,23 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
       x1.a = ldg16(a + 512);
       // KSEL >= 5 (theta = 0, d < 16): ref_off == 0, the reference row is the anchor row
       const uint8_t* r = ksel_c0_is_anchor<KSEL>() ? a : rbase0 + roff + lane16;
+      if constexpr (kNbrShfl) {
+        // the one narrow word of the window comes from the neighbour lane at
+        // vote time (nbr_fix); only the batch's boundary lane loads it
+        x0.mask = kNbrPending;
+        if constexpr (KSEL == 3) {
+          x0.c1 = ldg16(r + 16);
+          x1.c1 = ldg16(r + 528);
+          if (lane == 0) x0.c0.w = __ldg(reinterpret_cast<const uint32_t*>(r + 12));
+        } else {
+          if constexpr (KSEL == 0) {
+            x0.c0 = ldg16(r);
+            x1.c0 = ldg16(r + 512);
+          }
+          if (lane == 31) x1.c1.x = __ldg(reinterpret_cast<const uint32_t*>(r + 528));
+        }
+        return;
+      }
       if constexpr (!ksel_c0_is_anchor<KSEL>()) {
         x0.c0 = ldg16(r);
         x1.c0 = ldg16(r + 512);
@@ -845,6 +895,7 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
       }
       return;
     }
+    if constexpr (kNbrShfl) x0.mask = 0;
     const uint32_t off0 = lane16 + (jj0 + lane >= ni ? wrap_off : 0u);  // ni >= 64: at most one wrap
     const uint32_t off1 = lane16 + 512u + (jj0 + lane + 32u >= ni ? wrap_off : 0u);
     const uint8_t* a = abase0 + roff;
@@ -1039,22 +1090,26 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
   // one ticket grab (4 double batches) per two revolutions of the ring
   for (;;) {
     if (ta >= n_full_dbl) break;
+    nbr_fix(a0, a1);
     vote_full(a0);
     vote_full(a1);
     const uint32_t tn = grab4();
     ta = tn;
     if (ta < n_full_dbl) issue_dbl(mbeg + ta * 64, a0, a1);
     if (tb >= n_full_dbl) break;
+    nbr_fix(b0i, b1i);
     vote_full(b0i);
     vote_full(b1i);
     tb = tn + 1;
     if (tb < n_full_dbl) issue_dbl(mbeg + tb * 64, b0i, b1i);
     if (ta >= n_full_dbl) break;
+    nbr_fix(a0, a1);
     vote_full(a0);
     vote_full(a1);
     ta = tn + 2;
     if (ta < n_full_dbl) issue_dbl(mbeg + ta * 64, a0, a1);
     if (tb >= n_full_dbl) break;
+    nbr_fix(b0i, b1i);
     vote_full(b0i);
     vote_full(b1i);
     tb = tn + 3;
@@ -1098,11 +1153,13 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
         if (gb != kNone) issue_dbl(gb, b0i, b1i);
       }
       while (ga != kNone) {
+        nbr_fix(a0, a1);
         vote_full(a0);
         vote_full(a1);
         ga = gb == kNone ? kNone : grab_pool();
         if (ga != kNone) issue_dbl(ga, a0, a1);
         if (gb == kNone) break;
+        nbr_fix(b0i, b1i);
         vote_full(b0i);
         vote_full(b1i);
         gb = ga == kNone ? kNone : grab_pool();
