@@ -507,6 +507,17 @@ VotePrep prepare_vote(const uint8_t* d_img, size_t width, size_t height, size_t 
   return v;
 }
 
+// Fewest 16-pixel items per CTA (caps the grid of small images; a CTA's
+// fixed cost is its histogram zeroing and merge). TEXFORGE_MIN_CTA_ITEMS
+// overrides it for A/B timing.
+long long min_cta_items() {
+  static const long long v = [] {
+    const char* e = std::getenv("TEXFORGE_MIN_CTA_ITEMS");
+    return e ? std::max(32ll, std::atoll(e)) : 512ll;  // c1 (512^2): 21.3 -> 25.5 Gpairs/s vs 2048
+  }();
+  return v;
+}
+
 // Multi-job launches (glcm_vote_jobs_kernel); TEXFORGE_JOBS=0 launches every
 // (d, theta) on its own for A/B timing.
 bool jobs_enabled() {
@@ -567,7 +578,7 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
   }();
   long long per = units < slots ? std::max<long long>(1, slots / units)
                                 : std::max<long long>(1, (waves * slots + units - 1) / units);
-  per = std::max<long long>(1, std::min<long long>(per, (max_items + 2 * tfg::kThreads - 1) / (2 * tfg::kThreads)));
+  per = std::max<long long>(1, std::min<long long>(per, (max_items + min_cta_items() - 1) / min_cta_items()));
   if (units > 65535) return false;
   for (int j = 0; j < m; ++j) {
     tfg::VoteParams& p = jp.job[j];
@@ -634,7 +645,7 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
   const long long slots = (long long)ctx->num_sms * bps;
   long long per_band = n_bands < slots ? std::max<long long>(1, slots / std::max(n_bands, 1))
                                        : std::max<long long>(1, (8 * slots + n_bands - 1) / n_bands);
-  per_band = std::min<long long>(per_band, (p.items + 2 * tfg::kThreads - 1) / (2 * tfg::kThreads));
+  per_band = std::min<long long>(per_band, (p.items + min_cta_items() - 1) / min_cta_items());
   per_band = std::max<long long>(per_band, 1);
   const bool use_partials = cells > 4096;
   // With partials and a grid that is co-resident (one CTA per SM slot), the
