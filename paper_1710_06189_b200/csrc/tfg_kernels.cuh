@@ -832,9 +832,11 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
   // instead of a 4-byte load per lane (a strided LDG.32 touches the same 4-5
   // L1 lines as a full LDG.128).
   // Enabled for COPIES8 (L <= 64), whose kernel is bound by the L1 data pipe
-  // (noise L=64: -3..-6% per call); the issue-bound layouts (COPIES32 and
-  // PACKED16 on smooth input) lose more to the extra shuffles than they gain.
-  constexpr bool kNbrShfl = TFG_NBR_SHFL && STRAT == S_COPIES8 && (KSEL == 5 || KSEL == 0 || KSEL == 3);
+  // (noise L=64: -3..-6% per call), and for the one-slot PACKED16 variants
+  // (KSEL 0 and 3) outside run-length mode (noise warps: theta=45 -3.6%);
+  // the issue-bound paths (COPIES32, smooth PACKED16 warps) keep the loads.
+  constexpr bool kNbrShfl = TFG_NBR_SHFL && (KSEL == 5 || KSEL == 0 || KSEL == 3) &&
+                            (STRAT == S_COPIES8 || (STRAT == S_PACKED16 && KSEL != 5));
   constexpr uint32_t kNbrPending = 0x10000u;  // RawItem.mask of a main-pass x0 (vote_full ignores masks)
   auto nbr_fix = [&](RawItem& x0, RawItem& x1) {
     if constexpr (kNbrShfl) {
@@ -868,7 +870,7 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
       x1.a = ldg16(a + 512);
       // KSEL >= 5 (theta = 0, d < 16): ref_off == 0, the reference row is the anchor row
       const uint8_t* r = ksel_c0_is_anchor<KSEL>() ? a : rbase0 + roff + lane16;
-      if constexpr (kNbrShfl) {
+      if (kNbrShfl && !(STRAT == S_PACKED16 && rle)) {
         // the one narrow word of the window comes from the neighbour lane at
         // vote time (nbr_fix); only the batch's boundary lane loads it
         x0.mask = kNbrPending;
@@ -885,6 +887,7 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
         }
         return;
       }
+      if constexpr (kNbrShfl) x0.mask = 0;
       if constexpr (!ksel_c0_is_anchor<KSEL>()) {
         x0.c0 = ldg16(r);
         x1.c0 = ldg16(r + 512);
