@@ -1390,6 +1390,7 @@ int tfg_glcm_shard_jobs(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t bu
       band_words += (size_t)levels[t] * levels[t];
     }
     const size_t words = n_bands * band_words;
+    if (words > (size_t)INT32_MAX) fail(TFG_INVALID_ARGUMENT, "glcm_shard_jobs: too many output cells for one call");
     auto* d_acc = static_cast<unsigned long long*>(ctx->acc.get(words * 8));
     ck(cudaMemsetAsync(d_acc, 0, words * 8, s), "memset");
     if (owned_rows > 0) {
