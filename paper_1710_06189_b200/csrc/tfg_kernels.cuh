@@ -6,6 +6,9 @@
 //    R/include/texforge/glcm.hpp:110-130 (vote_anchor_rows) exactly:
 //    anchors in rows [0, min(row_end, H - drow)), columns
 //    [d*[dcol<0], W - d*[dcol>0]), cell = ref*L + anchor.
+// K1J glcm_vote_jobs_kernel: up to 8 (L, d, theta) jobs of one image or band
+//    batch in one launch (layouts without per-CTA partials, L <= 64); the
+//    same vote_cta body, the reference-window variant picked per CTA.
 // K0 glcm_vote_global_kernel: Scheme 1 (one global atomic per pair,
 //    PAPER.md:62-93 / parallel.hpp:121-152) — ablation only.
 // K3 symmetrize / normalize, K4 features — post-processing on device.
@@ -16,16 +19,23 @@
 // (lanes l and l+32; every LDG.128 of the warp is one coalesced 512-byte
 // access), four per grab from a per-CTA ticket counter and then, when the
 // launch is cooperative, from the band's shared tail pool; two double batches
-// sit in a register ring. An edge pass votes the row ends with masks. The reference
+// sit in a register ring (one for the PACKED16 variants with two reference
+// segments). An edge pass votes the row ends with masks. The reference
 // neighbour of each segment is one or two aligned 16-byte loads + funnel
 // shifts (displacement dcol = 16q + 4k + s: q and the word shift k are launch
-// / template constants, s is a byte funnel shift).
+// / template constants, s is a byte funnel shift); a window's one narrow word
+// comes from the adjacent lane by shuffle where the L1 data pipe binds
+// (nbr_fix). Interior segments start on 128-byte lines when the rows do.
 //
 // The vote itself is 3 instructions for L <= 128: the quantised anchor and
 // reference bytes are pre-scaled so that ONE byte permute (PRMT) of an anchor
 // word and a reference word gives a pixel pair's shared-memory offset, then
 // one IMAD adds the lane's copy base and one red.shared.add (ATOMS.POPC.INC)
 // casts the vote; 6 for the packed-u16 L=256 layout (kDrainBit).
+//
+// Measured A/B variants kept behind flags: TFG_TMA (TMA-staged
+// main pass), S_P16X16 (16 bank-pair copies for L <= 64), TFG_LDG_MODE
+// (L2-only loads), TFG_THREADS (CTA size).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
