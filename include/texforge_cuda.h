@@ -180,7 +180,10 @@ int tfg_glcm_shard(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t buffer_
 
 /*
  * tfg_glcm_shard with per-job levels: job t = (levels[t], distances[t],
- * angles_deg[t]); every band of the HOST image is copied up once and all its
+ * angles_deg[t]). Replaces a loop of the reference's compute_glcm_chunked /
+ * compute_glcm_serial calls over (L, d, theta) on one image
+ * (R/include/texforge/pipeline.hpp:246, glcm.hpp:144; R/tools/texforge.cpp:
+ * 218-236 loops them): every band of the HOST image is copied up once and all its
  * jobs vote from that copy (jobs that share a kernel instantiation in one
  * launch). counts_out: [band][job][levels[t]^2] u64, jobs back to back.
  * Counts only (no post-processing flags). n_jobs <= 64.
@@ -252,7 +255,8 @@ int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
 
 /*
  * Several GLCMs of one device image (or band batch) with per-job levels and
- * (d, theta): equivalent to n_jobs tfg_glcm_async calls, job t's counts at
+ * (d, theta) — a batch of compute_glcm_serial calls (R/include/texforge/
+ * glcm.hpp:144): equivalent to n_jobs tfg_glcm_async calls, job t's counts at
  * d_counts + sum_{u<t} n_bands * levels[u]^2 (band-major). Jobs that share a
  * kernel instantiation (L <= 64, same quantiser and layout) run as one
  * launch of up to 8 jobs. Stream-ordered like tfg_glcm_multi_async.
