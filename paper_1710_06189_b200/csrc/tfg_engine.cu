@@ -530,8 +530,9 @@ bool jobs_enabled() {
 
 // Enqueues n (d, theta) votes of the same image (or band batch) as ONE
 // glcm_vote_jobs_kernel launch: job t adds into d_counts + t * per_dt (band
-// b at + b * L^2). Only for the layouts without per-CTA partials (L <= 64);
-// returns false when it does not apply and the caller launches per (d, theta).
+// b at + b * L^2). Layouts with per-CTA partials (L > 64) go out as one
+// cooperative launch when the (job, band) rows fit one wave; returns false
+// when it does not apply and the caller launches per (d, theta).
 bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
                       size_t band_stride, int n_bands, size_t row_end, int pixel_levels, const int* levels,
                       const int* distances, const int* angles, unsigned long long* const* outs, int n,
@@ -541,7 +542,6 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
   int quant = -1, strat = -1;
   size_t words = 0;
   for (int t = 0; t < n; ++t) {
-    if ((size_t)levels[t] * levels[t] > 4096) return false;
     uint32_t qm = 0;
     int qs = 0;
     const int q = quant_mode(pixel_levels, levels[t], &qm, &qs);
@@ -572,6 +572,50 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
   // one wave of CTAs split evenly over the (job, band) units (launch_vote's rule per unit)
   const long long units = (long long)m * n_bands;
   const long long slots = (long long)ctx->num_sms * bps;
+  // L > 64 layouts (per-CTA partials): one cooperative launch, every unit's
+  // partials reduced in-kernel behind one grid barrier; the grid must be
+  // co-resident and every unit needs its own pool counter
+  const bool partials = strat == tfg::S_PACKED16 || strat == tfg::S_COPY1;
+  if (partials) {
+    static const bool coop = [] {
+      const char* e = std::getenv("TEXFORGE_COOP");
+      const char* j = std::getenv("TEXFORGE_JOBS_COOP");  // A/B knob: 0 = per-(d, theta) launches at L > 64
+      return !(e && e[0] == '0') && !(j && j[0] == '0');
+    }();
+    if (!coop || units > slots || units > kMaxPoolBands) return false;
+    const long long per = std::max<long long>(
+        1, std::min<long long>(slots / units, (max_items + min_cta_items() - 1) / min_cta_items()));
+    const bool packed = strat == tfg::S_PACKED16;
+    const size_t per_cta = packed ? words : (size_t)jp.job[0].levels * jp.job[0].levels;
+    for (int j = 0; j < m; ++j)  // one partial size per launch
+      if (jp.job[j].levels != jp.job[0].levels) return false;
+    tfg::VoteParams* ps = jp.job;
+    ScratchOrder order(ctx, s, true);
+    uint32_t* scratch = static_cast<uint32_t*>(ctx->partials.get((size_t)per * units * per_cta * 4));
+    for (int j = 0; j < m; ++j) {
+      tfg::VoteParams& p = ps[j];
+      const long long pool = p.main_items * pool_pct() / 100 / 256 * 4;  // whole grabs
+      p.pool_dbl = (uint32_t)std::min<long long>(pool, 1 << 24);
+      p.pool_beg = p.main_items - 64LL * p.pool_dbl;
+      p.pool_ctr = ctx->sync_ctr + kPoolCtrOffset;
+      p.sync_ctr = ctx->sync_ctr;
+      p.partials = scratch;
+      p.main_per_cta = ((p.pool_beg + per - 1) / per + 63) / 64 * 64;
+      p.edge_per_cta = (p.edge_items + per - 1) / per;
+    }
+    jp.nbands = n_bands;
+    jp.njobs = m;
+    void* args[] = {&jp};
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3((unsigned)per, (unsigned)units),
+                                                      dim3(tfg::kThreads), args, smem, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      cudaMemsetAsync(ctx->sync_ctr, 0, (kPoolCtrOffset + kMaxPoolBands) * sizeof(unsigned int), s);
+      ck(e, "glcm_vote_jobs_kernel cooperative launch");
+    }
+    ctx->launches++;
+    return true;
+  }
   static const long long waves = [] {
     const char* e = std::getenv("TEXFORGE_JOBS_WAVES");  // A/B knob: CTA waves when units exceed the SM slots
     return e ? std::max(1ll, std::atoll(e)) : 8ll;

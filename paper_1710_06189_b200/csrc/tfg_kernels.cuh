@@ -731,7 +731,11 @@ __device__ __forceinline__ void reduce_partials_slice(const VoteParams& p, uint3
 // vote_cta: the work of CTA `cta` of band `band_idx` (glcm_vote_kernel: the
 // block's x and y; glcm_vote_jobs_kernel: one job's share of the grid).
 template <int QUANT, int STRAT, int KSEL>
-__device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta, const int band_idx) {
+//
+// `unit` indexes the launch's scratch (per-CTA partials, pool counters): the
+// band for glcm_vote_kernel, the grid row (job x band) for the jobs kernel.
+__device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta, const int band_idx,
+                                         const int unit) {
   extern __shared__ __align__(16) uint32_t hist[];
   __shared__ uint32_t s_ticket;
   constexpr uint32_t kWarps = kThreads / 32;
@@ -1000,7 +1004,7 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
           if constexpr (STRAT == S_PACKED16 || STRAT == S_COPY1) {
             uint32_t g = kNone;
             if (lane == 0 && p.pool_ctr) {
-              const uint32_t tp = atomicAdd(p.pool_ctr + band_idx, 4u);
+              const uint32_t tp = atomicAdd(p.pool_ctr + unit, 4u);
               if (tp < p.pool_dbl) g = (uint32_t)p.pool_beg + tp * 64;
             }
             g = __shfl_sync(0xffffffffu, g, 0);
@@ -1129,7 +1133,7 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
         if (gleft == 0) {
           uint32_t g = kNone;
           if (lane == 0) {
-            const uint32_t tp = atomicAdd(p.pool_ctr + band_idx, 4u);
+            const uint32_t tp = atomicAdd(p.pool_ctr + unit, 4u);
             if (tp < p.pool_dbl) g = (uint32_t)p.pool_beg + tp * 64;
           }
           g = __shfl_sync(0xffffffffu, g, 0);
@@ -1210,7 +1214,7 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
         if (gleft == 0) {
           uint32_t g = kNone;
           if (lane == 0) {
-            const uint32_t tp = atomicAdd(p.pool_ctr + band_idx, kGrab);
+            const uint32_t tp = atomicAdd(p.pool_ctr + unit, kGrab);
             if (tp < p.pool_dbl) g = (uint32_t)p.pool_beg + tp * 64;
           }
           g = __shfl_sync(0xffffffffu, g, 0);
@@ -1287,11 +1291,11 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
   // (reduce_partials_slice); otherwise glcm_reduce_*_kernel does it.
   if (p.partials) {
     if constexpr (STRAT == S_PACKED16) {
-      uint4* dst = reinterpret_cast<uint4*>(p.partials + ((size_t)band_idx * gridDim.x + blockIdx.x) * (size_t)p.hist_words);
+      uint4* dst = reinterpret_cast<uint4*>(p.partials + ((size_t)unit * gridDim.x + blockIdx.x) * (size_t)p.hist_words);
       const uint4* src = reinterpret_cast<const uint4*>(hist);
       for (int i = tid; i < (p.hist_words >> 2); i += kThreads) dst[i] = src[i];
     } else {
-      uint32_t* part = p.partials + ((size_t)band_idx * gridDim.x + blockIdx.x) * (size_t)cells;
+      uint32_t* part = p.partials + ((size_t)unit * gridDim.x + blockIdx.x) * (size_t)cells;
       constexpr int RC = strat_copies(STRAT);
       for (int c = tid; c < cells; c += kThreads) {
         const uint32_t b = (uint32_t)c / L, a = (uint32_t)c - b * L;
@@ -1305,7 +1309,7 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
     if (p.sync_ctr) {
       const unsigned int n = gridDim.x * gridDim.y;
       grid_barrier(p.sync_ctr, n);
-      reduce_partials_slice<STRAT == S_PACKED16>(p, hist, band_idx, glcm);
+      reduce_partials_slice<STRAT == S_PACKED16>(p, hist, unit, glcm);
       // The last CTA out re-arms the counters for the next launch on the
       // stream (every CTA has left the barrier spin and the pool by now), so
       // the host needs no memset per launch.
@@ -1346,15 +1350,16 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
 
 template <int QUANT, int STRAT, int KSEL>
 __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams p) {
-  vote_cta<QUANT, STRAT, KSEL>(p, blockIdx.x, blockIdx.y);
+  vote_cta<QUANT, STRAT, KSEL>(p, blockIdx.x, blockIdx.y, blockIdx.y);
 }
 
 // Several (d, theta) GLCMs of one image (or band batch) in ONE launch: grid
 // row y = band * njobs + job, x = the job's CTAs. Each job keeps its own
 // geometry; the reference-window variant (KSEL) is picked per CTA, so all
 // of an image's angles share one launch and its fixed costs (SURVEY.md §7
-// "small images are latency-bound"). Layouts without per-CTA partials
-// (L <= 64) only: those end in direct u64 atomics, not a grid barrier.
+// "small images are latency-bound"). Layouts with per-CTA partials (L > 64)
+// run it as a cooperative launch: each (job, band) row has its own partials,
+// pool counter and reduce slices; one grid barrier for the whole launch.
 constexpr int kMaxJobs = 8;
 struct VoteJobs {
   VoteParams job[kMaxJobs];
@@ -1371,15 +1376,15 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_jobs_kernel(const __gri
   const int j = (int)blockIdx.y - band * jp.njobs;
   const VoteParams& p = jp.job[j];
   switch (jp.ksel[j]) {
-    case 0: vote_cta<QUANT, STRAT, 0>(p, blockIdx.x, band); break;
-    case 1: vote_cta<QUANT, STRAT, 1>(p, blockIdx.x, band); break;
-    case 2: vote_cta<QUANT, STRAT, 2>(p, blockIdx.x, band); break;
-    case 3: vote_cta<QUANT, STRAT, 3>(p, blockIdx.x, band); break;
-    case 5: vote_cta<QUANT, STRAT, 5>(p, blockIdx.x, band); break;
-    case 6: vote_cta<QUANT, STRAT, 6>(p, blockIdx.x, band); break;
-    case 7: vote_cta<QUANT, STRAT, 7>(p, blockIdx.x, band); break;
-    case 8: vote_cta<QUANT, STRAT, 8>(p, blockIdx.x, band); break;
-    default: vote_cta<QUANT, STRAT, 4>(p, blockIdx.x, band); break;
+    case 0: vote_cta<QUANT, STRAT, 0>(p, blockIdx.x, band, blockIdx.y); break;
+    case 1: vote_cta<QUANT, STRAT, 1>(p, blockIdx.x, band, blockIdx.y); break;
+    case 2: vote_cta<QUANT, STRAT, 2>(p, blockIdx.x, band, blockIdx.y); break;
+    case 3: vote_cta<QUANT, STRAT, 3>(p, blockIdx.x, band, blockIdx.y); break;
+    case 5: vote_cta<QUANT, STRAT, 5>(p, blockIdx.x, band, blockIdx.y); break;
+    case 6: vote_cta<QUANT, STRAT, 6>(p, blockIdx.x, band, blockIdx.y); break;
+    case 7: vote_cta<QUANT, STRAT, 7>(p, blockIdx.x, band, blockIdx.y); break;
+    case 8: vote_cta<QUANT, STRAT, 8>(p, blockIdx.x, band, blockIdx.y); break;
+    default: vote_cta<QUANT, STRAT, 4>(p, blockIdx.x, band, blockIdx.y); break;
   }
 }
 

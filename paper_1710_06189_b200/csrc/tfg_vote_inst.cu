@@ -42,13 +42,15 @@ VoteKernel TFG_CAT(tfg_pick_vote_q, TFG_QUANT)(int strat, int ksel) {
 }
 
 using JobsKernel = void (*)(const tfg::VoteJobs);
-// the multi-job kernel of a layout without per-CTA partials (nullptr otherwise)
+// the multi-job kernel of a layout (layouts with per-CTA partials: cooperative launches only)
 JobsKernel TFG_CAT(tfg_pick_jobs_q, TFG_QUANT)(int strat) {
   constexpr int Q = TFG_QUANT;
   switch (strat) {
     case tfg::S_COPIES32: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_COPIES32>;
     case tfg::S_COPIES8: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_COPIES8>;
     case tfg::S_P16X16: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_P16X16>;
+    case tfg::S_COPY1: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_COPY1>;
+    case tfg::S_PACKED16: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_PACKED16>;
     default: return nullptr;
   }
 }

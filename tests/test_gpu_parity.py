@@ -525,6 +525,39 @@ def test_jobs_launch_every_window(engine, levels, prequant, w):
             assert np.array_equal(got[0, t].reshape(-1), want), (dts, d, a)
 
 
+@pytest.mark.parametrize("levels,prequant,nb", [(100, False, 1), (256, False, 1), (200, True, 2), (256, False, 3)])
+def test_jobs_cooperative_partials(engine, levels, prequant, nb):
+    # L > 64 (COPY1 / PACKED16, per-CTA partials): up to 8 (d, theta) of one
+    # image or band batch go out as ONE cooperative glcm_vote_jobs_kernel
+    # launch; each (job, band) row keeps its own partials, pool counter and
+    # reduce slices behind the shared grid barrier. 12 pairs -> 2 launches.
+    import torch
+    w, h = 1296, 260  # pitch % 16 == 0 (the async ABI's alignment rule)
+    imgs = [(tf.synth_noise if b % 2 == 0 else tf.synth_smooth)(w, h, 90 + b).pixels for b in range(nb)]
+    px = [O.quantize(g, levels) if prequant else g for g in imgs]
+    dts = [(d, a) for d in (1, 2, 7) for a in (0, 45, 90, 135)]
+    dev = torch.from_numpy(np.concatenate(px)).cuda()
+    n = len(dts)
+    lv = (C.c_int * n)(*([levels] * n))
+    dd = (C.c_int * n)(*[d for d, _ in dts])
+    aa = (C.c_int * n)(*[a for _, a in dts])
+    out = torch.zeros(n * nb * levels * levels, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+    for rep in range(2):  # the second launch reuses the re-armed counters and scratch
+        out.zero_()
+        before = engine.launches
+        L.check(engine._lib.tfg_glcm_jobs_async(engine.handle, C.c_void_p(dev.data_ptr()), w, h, w, w * h, nb, h,
+                                                levels if prequant else 256, lv, dd, aa, n, 0,
+                                                C.c_void_p(out.data_ptr()), C.c_void_p(s.cuda_stream)))
+        # + the range check of a pre-quantised image (launch_validate)
+        assert engine.launches - before == 2 + int(prequant)
+        got = out.cpu().numpy().view(np.uint64).reshape(n, nb, -1)
+        for t, (d, a) in enumerate(dts):
+            for b in range(nb):
+                want = O.glcm_gray(imgs[b], w, h, levels, d, a)
+                assert np.array_equal(got[t, b], want), (rep, levels, d, a, b)
+
+
 @pytest.mark.parametrize("nb", [1, 3])
 def test_jobs_async_mixed_levels(engine, nb):
     # tfg_glcm_jobs_async: per-job (L, d, theta) of one device image / band
