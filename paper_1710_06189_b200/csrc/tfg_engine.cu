@@ -233,6 +233,10 @@ JobsKernel tfg_pick_jobs_q0(int strat);
 JobsKernel tfg_pick_jobs_q1(int strat);
 JobsKernel tfg_pick_jobs_q2(int strat);
 JobsKernel tfg_pick_jobs_q3(int strat);
+JobsKernel tfg_pick_jobs1_q0(int strat, int ksel);
+JobsKernel tfg_pick_jobs1_q1(int strat, int ksel);
+JobsKernel tfg_pick_jobs1_q2(int strat, int ksel);
+JobsKernel tfg_pick_jobs1_q3(int strat, int ksel);
 namespace {
 JobsKernel pick_jobs(int quant, int strat) {
   switch (quant) {
@@ -240,6 +244,14 @@ JobsKernel pick_jobs(int quant, int strat) {
     case tfg::Q_CLAMP: return tfg_pick_jobs_q1(strat);
     case tfg::Q_SHIFT: return tfg_pick_jobs_q2(strat);
     default: return tfg_pick_jobs_q3(strat);
+  }
+}
+JobsKernel pick_jobs1(int quant, int strat, int ksel) {
+  switch (quant) {
+    case tfg::Q_NONE: return tfg_pick_jobs1_q0(strat, ksel);
+    case tfg::Q_CLAMP: return tfg_pick_jobs1_q1(strat, ksel);
+    case tfg::Q_SHIFT: return tfg_pick_jobs1_q2(strat, ksel);
+    default: return tfg_pick_jobs1_q3(strat, ksel);
   }
 }
 
@@ -551,8 +563,7 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
     strat = st;
     words = std::max(words, hist_words_of(st, levels[t]));
   }
-  JobsKernel fn = pick_jobs(quant, strat);
-  if (!fn) return false;
+  const bool partials = strat == tfg::S_PACKED16 || strat == tfg::S_COPY1;
   const size_t smem = words * 4 + tfg::kTmaBytes;
   tfg::VoteJobs jp{};
   int m = 0;
@@ -568,6 +579,11 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
     ++m;
   }
   if (m == 0) return true;
+  // partial layouts: one KSEL per launch (glcm_vote_jobs1_kernel; launch_job_set groups by it)
+  for (int j = 1; j < m && partials; ++j)
+    if (jp.ksel[j] != jp.ksel[0]) return false;
+  JobsKernel fn = partials ? pick_jobs1(quant, strat, jp.ksel[0]) : pick_jobs(quant, strat);
+  if (!fn) return false;
   const int bps = occupancy_for(reinterpret_cast<const void*>(fn), smem);
   // one wave of CTAs split evenly over the (job, band) units (launch_vote's rule per unit)
   const long long units = (long long)m * n_bands;
@@ -575,7 +591,6 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
   // L > 64 layouts (per-CTA partials): one cooperative launch, every unit's
   // partials reduced in-kernel behind one grid barrier; the grid must be
   // co-resident and every unit needs its own pool counter
-  const bool partials = strat == tfg::S_PACKED16 || strat == tfg::S_COPY1;
   if (partials) {
     static const bool coop = [] {
       const char* e = std::getenv("TEXFORGE_COOP");
@@ -637,7 +652,13 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
   return true;
 }
 
+void launch_job_set(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
+                    size_t band_stride, int n_bands, size_t row_end, int pixel_levels, const int* levels,
+                    const int* distances, const int* angles, unsigned long long* const* outs, int n_jobs,
+                    unsigned flags, cudaStream_t s);
+
 // The common case: n (d, theta) at one L, job t adding into d_counts + t * per_dt.
+// L > 64: the jobs go out grouped by KSEL (launch_job_set), so this returns true.
 bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
                       size_t band_stride, int n_bands, size_t row_end, int pixel_levels, int levels,
                       const int* distances, const int* angles, int n, unsigned flags, unsigned long long* d_counts,
@@ -648,6 +669,11 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
   for (int t = 0; t < n; ++t) {
     lv[t] = levels;
     outs[t] = d_counts + (size_t)t * per_dt;
+  }
+  if ((size_t)levels * levels > 4096 && !(flags & TFG_SCHEME_GLOBAL) && jobs_enabled()) {
+    launch_job_set(ctx, d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels, lv, distances,
+                   angles, outs, n, flags, s);
+    return true;
   }
   return launch_vote_jobs(ctx, d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels, lv, distances,
                           angles, outs, n, flags, s);
@@ -767,23 +793,59 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
 }
 
 // Enqueues jobs with per-job (L, d, theta), job t adding into outs[t] (band b
-// at + b * L_t^2): runs that share a kernel instantiation go out as one
-// multi-job launch of up to kMaxJobs, the rest one launch per job (all
-// ordered on `s`).
+// at + b * L_t^2). Jobs that share a kernel instantiation go out as multi-job
+// launches of up to kMaxJobs, in any order: the key is (quantiser, layout)
+// and, for the layouts with per-CTA partials, also (L, KSEL) — one partial
+// size and one KSEL per glcm_vote_jobs1_kernel launch. Singletons and jobs
+// no multi-job launch takes get one launch each (all ordered on `s`).
 void launch_job_set(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
                     size_t band_stride, int n_bands, size_t row_end, int pixel_levels, const int* levels,
                     const int* distances, const int* angles, unsigned long long* const* outs, int n_jobs,
                     unsigned flags, cudaStream_t s) {
-  int t = 0;
-  while (t < n_jobs) {
-    int n = std::min(n_jobs - t, tfg::kMaxJobs);
-    while (n > 1 && !launch_vote_jobs(ctx, d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels,
-                                       levels + t, distances + t, angles + t, outs + t, n, flags, s))
-      --n;
-    if (n == 1)
-      launch_vote(ctx, d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels, levels[t],
-                  distances[t], angles[t], flags, outs[t], s);
-    t += n;
+  std::vector<long long> key(n_jobs);
+  for (int t = 0; t < n_jobs; ++t) {
+    uint32_t qm = 0;
+    int qs = 0;
+    const int q = quant_mode(pixel_levels, levels[t], &qm, &qs);
+    const int st = pick_strategy(levels[t], flags);
+    long long k = q * 16 + st;
+    if (st == tfg::S_PACKED16 || st == tfg::S_COPY1) {
+      const VoteGeometry g = make_geometry(width, height, pitch, row_end, levels[t], pixel_levels, distances[t],
+                                           angles[t]);
+      k += 256LL * levels[t] + 65536LL * (g.ksel + 1);
+    }
+    key[t] = k;
+  }
+  std::vector<char> done(n_jobs, 0);
+  std::vector<int> idx;
+  for (int t = 0; t < n_jobs; ++t) {
+    if (done[t]) continue;
+    idx.clear();
+    for (int u = t; u < n_jobs; ++u)
+      if (!done[u] && key[u] == key[t]) {
+        idx.push_back(u);
+        done[u] = 1;
+      }
+    size_t i = 0;
+    while (i < idx.size()) {
+      int n = (int)std::min<size_t>(idx.size() - i, tfg::kMaxJobs);
+      int lv[tfg::kMaxJobs], dd[tfg::kMaxJobs], aa[tfg::kMaxJobs];
+      unsigned long long* oo[tfg::kMaxJobs];
+      for (int j = 0; j < n; ++j) {
+        const int u = idx[i + j];
+        lv[j] = levels[u];
+        dd[j] = distances[u];
+        aa[j] = angles[u];
+        oo[j] = outs[u];
+      }
+      while (n > 1 && !launch_vote_jobs(ctx, d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels,
+                                         lv, dd, aa, oo, n, flags, s))
+        --n;
+      if (n == 1)
+        launch_vote(ctx, d_img, width, height, pitch, band_stride, n_bands, row_end, pixel_levels, lv[0], dd[0],
+                    aa[0], flags, oo[0], s);
+      i += n;
+    }
   }
 }
 

@@ -1358,8 +1358,9 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_kernel(const VoteParams
 // geometry; the reference-window variant (KSEL) is picked per CTA, so all
 // of an image's angles share one launch and its fixed costs (SURVEY.md §7
 // "small images are latency-bound"). Layouts with per-CTA partials (L > 64)
-// run it as a cooperative launch: each (job, band) row has its own partials,
-// pool counter and reduce slices; one grid barrier for the whole launch.
+// run glcm_vote_jobs1_kernel as a cooperative launch: each (job, band) row
+// has its own partials, pool counter and reduce slices; one grid barrier for
+// the whole launch.
 constexpr int kMaxJobs = 8;
 struct VoteJobs {
   VoteParams job[kMaxJobs];
@@ -1367,6 +1368,18 @@ struct VoteJobs {
   int nbands;
   int njobs;
 };
+
+// One KSEL for every job of the launch: the layouts with per-CTA partials
+// (COPY1, PACKED16). With the per-job switch below, ptxas spills 100-240
+// bytes of the PACKED16 body (its nine inlined variants are allocated as one
+// function), which costs the issue-bound smooth path ~2.5%; this form is
+// spill-free and the host groups jobs by KSEL.
+template <int QUANT, int STRAT, int KSEL>
+__global__ void __launch_bounds__(kThreads, 1) glcm_vote_jobs1_kernel(const __grid_constant__ VoteJobs jp) {
+  const int band = (int)blockIdx.y / jp.njobs;
+  const int j = (int)blockIdx.y - band * jp.njobs;
+  vote_cta<QUANT, STRAT, KSEL>(jp.job[j], blockIdx.x, band, blockIdx.y);
+}
 
 template <int QUANT, int STRAT>
 __global__ void __launch_bounds__(kThreads, 1) glcm_vote_jobs_kernel(const __grid_constant__ VoteJobs jp) {

@@ -42,15 +42,40 @@ VoteKernel TFG_CAT(tfg_pick_vote_q, TFG_QUANT)(int strat, int ksel) {
 }
 
 using JobsKernel = void (*)(const tfg::VoteJobs);
-// the multi-job kernel of a layout (layouts with per-CTA partials: cooperative launches only)
+// the multi-job kernel of a layout without per-CTA partials (L <= 64)
 JobsKernel TFG_CAT(tfg_pick_jobs_q, TFG_QUANT)(int strat) {
   constexpr int Q = TFG_QUANT;
   switch (strat) {
     case tfg::S_COPIES32: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_COPIES32>;
     case tfg::S_COPIES8: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_COPIES8>;
     case tfg::S_P16X16: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_P16X16>;
-    case tfg::S_COPY1: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_COPY1>;
-    case tfg::S_PACKED16: return tfg::glcm_vote_jobs_kernel<Q, tfg::S_PACKED16>;
+    default: return nullptr;  // COPY1, PACKED16: tfg_pick_jobs1_q<N>
+  }
+}
+
+namespace {
+template <int Q, int S>
+JobsKernel pick_j1(int ksel) {
+  switch (ksel) {
+    case 0: return tfg::glcm_vote_jobs1_kernel<Q, S, 0>;
+    case 1: return tfg::glcm_vote_jobs1_kernel<Q, S, 1>;
+    case 2: return tfg::glcm_vote_jobs1_kernel<Q, S, 2>;
+    case 3: return tfg::glcm_vote_jobs1_kernel<Q, S, 3>;
+    case 5: return tfg::glcm_vote_jobs1_kernel<Q, S, 5>;
+    case 6: return tfg::glcm_vote_jobs1_kernel<Q, S, 6>;
+    case 7: return tfg::glcm_vote_jobs1_kernel<Q, S, 7>;
+    case 8: return tfg::glcm_vote_jobs1_kernel<Q, S, 8>;
+    default: return tfg::glcm_vote_jobs1_kernel<Q, S, 4>;
+  }
+}
+}  // namespace
+
+// the one-KSEL multi-job kernel of a layout with per-CTA partials (cooperative launches)
+JobsKernel TFG_CAT(tfg_pick_jobs1_q, TFG_QUANT)(int strat, int ksel) {
+  constexpr int Q = TFG_QUANT;
+  switch (strat) {
+    case tfg::S_COPY1: return pick_j1<Q, tfg::S_COPY1>(ksel);
+    case tfg::S_PACKED16: return pick_j1<Q, tfg::S_PACKED16>(ksel);
     default: return nullptr;
   }
 }
