@@ -975,9 +975,12 @@ def run_engine(args, wl):
                        "check": check},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": committed_traffic(wl),
-                         "kernel": "glcm_vote_kernel (+ its split-K partial reduce for L*L > 4096): one engine call",
-                         "bytes_per_launch": bytes_per_call, "launches_per_step": len(jobs),
-                         "basis": "bytes_per_launch x launches_per_step / ms_per_step (timed region, per GPU)",
+                         "kernel": ("glcm_vote_jobs_kernel / glcm_vote_jobs1_kernel (multi-(d, theta) launches; "
+                                    "glcm_vote_kernel for a lone (d, theta))"),
+                         "bytes_per_job": bytes_per_call, "jobs_per_step": len(jobs),
+                         "launches_per_step": gpu_launches / max(args.steps, 1),
+                         "basis": ("bytes_per_job x jobs_per_step / ms_per_step (timed region, per GPU); a job is one "
+                                   "(L, input, d, theta) over all its bands; traffic: ncu DRAM bytes per job"),
                          "per_call": {"avg_launch_ms": avg_ms, "achieved": per_call_achieved,
                                       "frac": per_call_achieved / peak,
                                       "how": "separate pass, CUDA events around each engine call on its stream"},

@@ -1,7 +1,9 @@
-// tfg_vote_inst.cu — the glcm_vote_kernel instantiations of one quantiser
+// tfg_vote_inst.cu — the vote kernel instantiations of one quantiser
 // (TFG_QUANT = tfg::Quant), compiled once per quantiser as tfg_vote_q<N>.o so
 // the four sets build in parallel. tfg_engine.cu dispatches through
-// tfg_pick_vote_q<N>(strat, ksel).
+// tfg_pick_vote_q<N>(strat, ksel) (glcm_vote_kernel), tfg_pick_jobs_q<N>(strat)
+// (glcm_vote_jobs_kernel, L <= 64) and tfg_pick_jobs1_q<N>(strat, ksel)
+// (glcm_vote_jobs1_kernel, L > 64).
 #define TFG_VOTE_ONLY
 #include "tfg_kernels.cuh"
 
