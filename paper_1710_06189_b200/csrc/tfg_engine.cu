@@ -246,6 +246,12 @@ JobsKernel pick_jobs(int quant, int strat) {
     default: return tfg_pick_jobs_q3(strat);
   }
 }
+// The KSELs one L > 64 multi-job launch may mix (glcm_vote_jobs2_kernel:
+// PACKED16 pairs {0,1} {2,3} {5,6} {7,8}; COPY1: one KSEL).
+int ksel_group(int strat, int ksel) {
+  if (strat != tfg::S_PACKED16 || ksel == 4) return ksel;
+  return ksel < 4 ? (ksel & ~1) : 5 + ((ksel - 5) & ~1);
+}
 JobsKernel pick_jobs1(int quant, int strat, int ksel) {
   switch (quant) {
     case tfg::Q_NONE: return tfg_pick_jobs1_q0(strat, ksel);
@@ -579,9 +585,9 @@ bool launch_vote_jobs(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t h
     ++m;
   }
   if (m == 0) return true;
-  // partial layouts: one KSEL per launch (glcm_vote_jobs1_kernel; launch_job_set groups by it)
+  // partial layouts: one KSEL group per launch (glcm_vote_jobs1/2_kernel; launch_job_set groups by it)
   for (int j = 1; j < m && partials; ++j)
-    if (jp.ksel[j] != jp.ksel[0]) return false;
+    if (ksel_group(strat, jp.ksel[j]) != ksel_group(strat, jp.ksel[0])) return false;
   JobsKernel fn = partials ? pick_jobs1(quant, strat, jp.ksel[0]) : pick_jobs(quant, strat);
   if (!fn) return false;
   const int bps = occupancy_for(reinterpret_cast<const void*>(fn), smem);
@@ -795,8 +801,8 @@ void launch_vote(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height
 // Enqueues jobs with per-job (L, d, theta), job t adding into outs[t] (band b
 // at + b * L_t^2). Jobs that share a kernel instantiation go out as multi-job
 // launches of up to kMaxJobs, in any order: the key is (quantiser, layout)
-// and, for the layouts with per-CTA partials, also (L, KSEL) — one partial
-// size and one KSEL per glcm_vote_jobs1_kernel launch. Singletons and jobs
+// and, for the layouts with per-CTA partials, also (L, KSEL group) — one
+// partial size and one KSEL group (ksel_group) per launch. Singletons and jobs
 // no multi-job launch takes get one launch each (all ordered on `s`).
 void launch_job_set(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t height, size_t pitch,
                     size_t band_stride, int n_bands, size_t row_end, int pixel_levels, const int* levels,
@@ -812,7 +818,7 @@ void launch_job_set(tfg_ctx* ctx, const uint8_t* d_img, size_t width, size_t hei
     if (st == tfg::S_PACKED16 || st == tfg::S_COPY1) {
       const VoteGeometry g = make_geometry(width, height, pitch, row_end, levels[t], pixel_levels, distances[t],
                                            angles[t]);
-      k += 256LL * levels[t] + 65536LL * (g.ksel + 1);
+      k += 256LL * levels[t] + 65536LL * (ksel_group(st, g.ksel) + 1);
     }
     key[t] = k;
   }

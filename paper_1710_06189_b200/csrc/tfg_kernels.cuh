@@ -1381,6 +1381,19 @@ __global__ void __launch_bounds__(kThreads, 1) glcm_vote_jobs1_kernel(const __gr
   vote_cta<QUANT, STRAT, KSEL>(jp.job[j], blockIdx.x, band, blockIdx.y);
 }
 
+// PACKED16: two neighbouring KSELs per launch ({0,1}, {2,3}, {5,6}, {7,8};
+// e.g. d = 1, 2 and 4 at 0 or 135 degrees), still spill-free with two
+// inlined bodies; KSEL 4 uses glcm_vote_jobs1_kernel.
+template <int QUANT, int STRAT, int K1, int K2>
+__global__ void __launch_bounds__(kThreads, 1) glcm_vote_jobs2_kernel(const __grid_constant__ VoteJobs jp) {
+  const int band = (int)blockIdx.y / jp.njobs;
+  const int j = (int)blockIdx.y - band * jp.njobs;
+  if (jp.ksel[j] == K1)
+    vote_cta<QUANT, STRAT, K1>(jp.job[j], blockIdx.x, band, blockIdx.y);
+  else
+    vote_cta<QUANT, STRAT, K2>(jp.job[j], blockIdx.x, band, blockIdx.y);
+}
+
 template <int QUANT, int STRAT>
 __global__ void __launch_bounds__(kThreads, 1) glcm_vote_jobs_kernel(const __grid_constant__ VoteJobs jp) {
   // band-major: the jobs of one band run side by side (adjacent blocks, the

@@ -3,7 +3,7 @@
 // the four sets build in parallel. tfg_engine.cu dispatches through
 // tfg_pick_vote_q<N>(strat, ksel) (glcm_vote_kernel), tfg_pick_jobs_q<N>(strat)
 // (glcm_vote_jobs_kernel, L <= 64) and tfg_pick_jobs1_q<N>(strat, ksel)
-// (glcm_vote_jobs1_kernel, L > 64).
+// (glcm_vote_jobs1/2_kernel, L > 64).
 #define TFG_VOTE_ONLY
 #include "tfg_kernels.cuh"
 
@@ -72,12 +72,22 @@ JobsKernel pick_j1(int ksel) {
 }
 }  // namespace
 
-// the one-KSEL multi-job kernel of a layout with per-CTA partials (cooperative launches)
+// the multi-job kernel of a layout with per-CTA partials (cooperative
+// launches) for a KSEL group (tfg_engine.cu ksel_group): COPY1 one KSEL,
+// PACKED16 a KSEL pair or KSEL 4
 JobsKernel TFG_CAT(tfg_pick_jobs1_q, TFG_QUANT)(int strat, int ksel) {
   constexpr int Q = TFG_QUANT;
+  constexpr int P = tfg::S_PACKED16;
   switch (strat) {
     case tfg::S_COPY1: return pick_j1<Q, tfg::S_COPY1>(ksel);
-    case tfg::S_PACKED16: return pick_j1<Q, tfg::S_PACKED16>(ksel);
+    case tfg::S_PACKED16:
+      switch (ksel) {
+        case 0: case 1: return tfg::glcm_vote_jobs2_kernel<Q, P, 0, 1>;
+        case 2: case 3: return tfg::glcm_vote_jobs2_kernel<Q, P, 2, 3>;
+        case 5: case 6: return tfg::glcm_vote_jobs2_kernel<Q, P, 5, 6>;
+        case 7: case 8: return tfg::glcm_vote_jobs2_kernel<Q, P, 7, 8>;
+        default: return tfg::glcm_vote_jobs1_kernel<Q, P, 4>;
+      }
     default: return nullptr;
   }
 }
