@@ -258,8 +258,9 @@ int tfg_glcm_multi_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t
  * (d, theta) — a batch of compute_glcm_serial calls (R/include/texforge/
  * glcm.hpp:144): equivalent to n_jobs tfg_glcm_async calls, job t's counts at
  * d_counts + sum_{u<t} n_bands * levels[u]^2 (band-major). Jobs that share a
- * kernel instantiation (L <= 64, same quantiser and layout) run as one
- * launch of up to 8 jobs. Stream-ordered like tfg_glcm_multi_async.
+ * kernel instantiation (same quantiser and layout; for L > 64 also the same L
+ * and reference-window group, as one cooperative launch) run as one launch
+ * of up to 8 jobs. Stream-ordered like tfg_glcm_multi_async.
  */
 int tfg_glcm_jobs_async(tfg_ctx* ctx, const uint8_t* d_px, size_t width, size_t height, size_t pitch,
                         size_t band_stride, size_t n_bands, size_t row_end, int pixel_levels, const int* levels,

@@ -8,8 +8,8 @@ for b in dropin_tests refsuite_unit refsuite_accept; do timeout 900 tests/cpp/_b
 timeout 900 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err
 timeout 600 python bench.py --impl reference > $O/bench_ref_c3.json 2> $O/bench_ref_c3.err
 for wl in c2 c4 c5 c1; do timeout 900 python bench.py --workload $wl --steps 10 --warmup 3 > $O/bench_$wl.json 2> $O/bench_$wl.err; done
-# one timed c3 step's launch list (12 launches: 6 KSEL groups x 2 images; cold, serialised: shares only)
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:glcm -s 48 -c 12 --csv --log-file $O/launches_c3.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launches.log 2>&1
+# one timed c3 step's launch list (8 launches: 4 KSEL groups x 2 images; cold, serialised: shares only)
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:glcm -s 32 -c 8 --csv --log-file $O/launches_c3.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launches.log 2>&1
 # ncu --set full of the dominant kernels: L=256 (c3) noise/smooth, L=64 (c5), L=32 (c4), the c2 jobs launch
 cap() { # name, profile_vote args
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:glcm_vote -c 1 -f -o $O/$1 python tools/profile_vote.py ${@:2} --reps 1 > $O/$1.log 2>&1
@@ -24,6 +24,7 @@ cap vote_L32_noise --levels 32 --kinds noise --dts 1:0
 cap jobs_c2_L32_noise --levels 32 --kinds noise --dts 1:0,1:45,1:90,1:135 --size 4096 --multi
 cap jobs1_c3_L256_noise --levels 256 --kinds noise --dts 1:90,2:90,4:90 --multi
 cap jobs1_c3_L256_smooth --levels 256 --kinds smooth --dts 1:90,2:90,4:90 --multi
+cap jobs2_c3_L256_noise --levels 256 --kinds noise --dts 1:0,2:0,4:0 --multi
 # K0 (Scheme 1, one global atomic per pair) ablation: the paper's contention trend
 for L in 8 32 256; do for K in noise smooth; do
   timeout 600 ncu --metrics gpu__time_duration.sum,lts__t_requests_op_red.sum,lts__t_sectors_op_red.sum,lts__average_t_sector_hit_rate_realtime.pct,l1tex__t_set_conflicts_pipe_lsu_mem_global_op_red.sum,lts__throughput.avg.pct_of_peak_sustained_elapsed --clock-control none -k regex:glcm_vote_global -c 1 --csv python tools/profile_vote.py --levels $L --kinds $K --dts 1:0 --size 4096 --scheme1 --reps 1 > $O/k0_L${L}_$K.csv 2>&1
