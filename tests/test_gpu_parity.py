@@ -561,6 +561,32 @@ def test_jobs_cooperative_partials(engine, levels, prequant, nb):
                 assert np.array_equal(got[t, b], want), (rep, levels, d, a, b)
 
 
+def test_jobs_cooperative_rows_exceed_one_wave(engine):
+    # 20 bands x 8 jobs of one KSEL (90 deg) = 160 (job, band) rows > 148 SM
+    # slots: the cooperative launch needs every row co-resident, so
+    # launch_job_set shrinks the launch to 7 jobs (140 rows) and the 8th job
+    # takes its own launch — 2 launches, every GLCM exact.
+    import torch
+    w, h, nb = 304, 40, 20
+    imgs = [(tf.synth_noise if b % 3 else tf.synth_smooth)(w, h, 120 + b).pixels for b in range(nb)]
+    dev = torch.from_numpy(np.concatenate(imgs)).cuda()
+    dts = [(d, 90) for d in range(1, 9)]
+    n = len(dts)
+    lv = (C.c_int * n)(*([256] * n))
+    dd = (C.c_int * n)(*[d for d, _ in dts])
+    aa = (C.c_int * n)(*[a for _, a in dts])
+    out = torch.zeros(n * nb * 65536, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+    before = engine.launches
+    L.check(engine._lib.tfg_glcm_jobs_async(engine.handle, C.c_void_p(dev.data_ptr()), w, h, w, w * h, nb, h, 256,
+                                            lv, dd, aa, n, 0, C.c_void_p(out.data_ptr()), C.c_void_p(s.cuda_stream)))
+    assert engine.launches - before == 2
+    got = out.cpu().numpy().view(np.uint64).reshape(n, nb, -1)
+    for t, (d, a) in enumerate(dts):
+        for b in range(nb):
+            assert np.array_equal(got[t, b], O.glcm_gray(imgs[b], w, h, 256, d, a)), (d, b)
+
+
 @pytest.mark.parametrize("nb", [1, 3])
 def test_jobs_async_mixed_levels(engine, nb):
     # tfg_glcm_jobs_async: per-job (L, d, theta) of one device image / band
