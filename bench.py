@@ -577,7 +577,7 @@ def run_engine(args, wl):
     if per_gpu_bytes < 2 * L2_BYTES:
         flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device="cuda")
     launches = []
-    record = {"on": False}
+    record = {"on": False, "single": False}  # single: one engine call per job; on: time each call
 
     # timed steps: one engine call per input with every (L, d, theta) of it
     # (tfg_glcm_jobs_async); the roofline pass below times single launches
@@ -623,7 +623,7 @@ def run_engine(args, wl):
                 Lb.check(rc)
 
     def vote_all():
-        if not record["on"]:
+        if not record["single"]:
             vote_grouped()
             return
         for j, (L, kind, d, a) in enumerate(jobs):
@@ -764,7 +764,13 @@ def run_engine(args, wl):
         dist.barrier()
     value = pairs_per_step / (ms / 1e3) / 1e9
 
-    # per-call durations for the roofline (separate pass, same stream)
+    # per-call durations for the roofline (separate pass, same stream); one
+    # untimed pass first: the timed steps may not have used the one-job
+    # kernels, and their first (lazy) module load would land in the events
+    record["single"] = True
+    acc.zero_()
+    vote_all()
+    torch.cuda.synchronize()
     record["on"] = True
     for s in range(max(2, min(args.steps, 5))):
         acc.zero_()
@@ -783,6 +789,17 @@ def run_engine(args, wl):
     # memset included, so this is the conservative figure). The separate
     # per-call pass above explains it (per_call).
     achieved = bytes_per_call * len(jobs) / (ms / 1e3) / 1e9
+    # SURVEY.md §8(d)'s clause for fused launches: "if one launch computes
+    # n_out (d, theta) pairs from a single read, the image bytes count once".
+    # Each engine call's launches each read its input once (c3: 4 launches
+    # per input, 3 (d, theta) each), so this basis credits far fewer bytes
+    # than the per-job one; reported beside it, not instead of it.
+    calls_per_step = 1 if merge_kinds else len(gargs)
+    launches_per_call = (gpu_launches / max(args.steps, 1)) / max(calls_per_step, 1)
+    input_bytes = sum((plan.bands * W * plan.height if plan.layout == "bands" else buf_rows[k] * W)
+                      for k in plan.kinds)
+    glcm_bytes = sum(plan.bands * cells[L] * 8 for (L, _k, _d, _a) in jobs)
+    read_once_achieved = (launches_per_call * input_bytes + glcm_bytes) / (ms / 1e3) / 1e9
 
     # end-to-end through the public C ABI from pinned host memory: H2D of this
     # step's inputs inside the region, counts back to the host, NCCL reduce
@@ -981,6 +998,10 @@ def run_engine(args, wl):
                          "launches_per_step": gpu_launches / max(args.steps, 1),
                          "basis": ("bytes_per_job x jobs_per_step / ms_per_step (timed region, per GPU); a job is one "
                                    "(L, input, d, theta) over all its bands; traffic: ncu DRAM bytes per job"),
+                         "read_once": {"achieved": read_once_achieved, "frac": read_once_achieved / peak,
+                                       "launches_per_call": launches_per_call,
+                                       "how": ("SURVEY.md §8(d) fused-launch basis: each launch's image bytes once "
+                                               "+ every GLCM write, over the timed region")},
                          "per_call": {"avg_launch_ms": avg_ms, "achieved": per_call_achieved,
                                       "frac": per_call_achieved / peak,
                                       "how": "separate pass, CUDA events around each engine call on its stream"},
