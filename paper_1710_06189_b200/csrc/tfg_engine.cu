@@ -1032,6 +1032,15 @@ std::vector<uint64_t> chunk_specs(size_t width, size_t height, const int* distan
 // the caller's own host rows.
 // `specs`: k chunks {owned_row_start, owned_row_end, buffer_row_end} (any
 // subset of a partition(): a GPU of a multi-GPU group runs its own chunks).
+// Row copies whose rows are contiguous on both sides (pitch == width) go
+// out as ONE linear copy instead of a pitched 2D copy (measured the same
+// for c2's 4096^2 images, tools/e2e_c2_diag.py; no per-row descriptors).
+inline cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+                             cudaMemcpyKind kind, cudaStream_t s) {
+  if (dpitch == width && spitch == width) return cudaMemcpyAsync(dst, src, width * rows, kind, s);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, s);
+}
+
 template <typename Fetch>
 void run_pipeline_specs(tfg_ctx* ctx, size_t width, const std::vector<uint64_t>& specs, int pixel_levels,
                         int levels, const int* distances, const int* angles, int n_dt, unsigned flags,
@@ -1048,6 +1057,7 @@ void run_pipeline_specs(tfg_ctx* ctx, size_t width, const std::vector<uint64_t>&
   for (size_t i = 0; i < k; ++i) max_rows = std::max<size_t>(max_rows, specs[3 * i + 2] - specs[3 * i]);
   const bool sequential = (flags & TFG_SEQUENTIAL) != 0;
   for (int sl = 0; sl < tfg_ctx::kSlots; ++sl) ctx->dslot[sl].get(max_rows * pitch + 64);
+  size_t pending_band = SIZE_MAX;  // band whose band_done waits for the next chunk's H2D
   for (size_t n = 0; n < n_bands * k; ++n) {
     const size_t bnd = n / k, i = n % k;
     const int sl = (int)(n % tfg_ctx::kSlots);
@@ -1059,8 +1069,15 @@ void run_pipeline_specs(tfg_ctx* ctx, size_t width, const std::vector<uint64_t>&
     uint8_t* dst = static_cast<uint8_t*>(ctx->dslot[sl].p);
     // device side: the slot's previous votes must be done before overwrite
     if (n >= (size_t)tfg_ctx::kSlots) ck(cudaStreamWaitEvent(ctx->copy, ctx->consumed[sl], 0), "wait");
-    ck(cudaMemcpy2DAsync(dst, pitch, src, width, width, rows, cudaMemcpyHostToDevice, ctx->copy), "H2D chunk");
+    ck(copy_rows(dst, pitch, src, width, width, rows, cudaMemcpyHostToDevice, ctx->copy), "H2D chunk");
     ck(cudaEventRecord(ctx->copied[sl], ctx->copy), "event record");
+    // the previous band's early counts D2H goes out only now, after this
+    // chunk's H2D: enqueued before it, its wait on that band's votes held
+    // this copy back (c2 e2e: 2 bands 1.06 -> 0.70 ms, tools/e2e_c2_diag.py)
+    if (pending_band != SIZE_MAX) {
+      band_done(pending_band);
+      pending_band = SIZE_MAX;
+    }
     ck(cudaStreamWaitEvent(ctx->exec, ctx->copied[sl], 0), "wait");
     if (pixel_levels == levels) launch_validate(ctx, dst, width, rows, pitch, 0, 1, levels, sync_err(ctx), ctx->exec);
     if (job_levels) {
@@ -1076,9 +1093,10 @@ void run_pipeline_specs(tfg_ctx* ctx, size_t width, const std::vector<uint64_t>&
                     angles[t], flags, d_acc + bnd * acc_band_stride + (size_t)t * levels * levels, ctx->exec);
     }
     ck(cudaEventRecord(ctx->consumed[sl], ctx->exec), "event record");
-    if (band_done && i == k - 1) band_done(bnd);
+    if (band_done && i == k - 1) pending_band = bnd;
     if (sequential) ck(cudaStreamSynchronize(ctx->exec), "stream sync");
   }
+  if (pending_band != SIZE_MAX) band_done(pending_band);
 }
 
 template <typename Fetch>
@@ -1102,7 +1120,7 @@ void stage_host_image(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t heig
                       size_t dpitch) {
   cudaStream_t s = ctx->exec;
   if (host_memory_kind(px) != 0) {
-    ck(cudaMemcpy2DAsync(d_dst, dpitch, px, width, width, height, cudaMemcpyHostToDevice, s), "stage image");
+    ck(copy_rows(d_dst, dpitch, px, width, width, height, cudaMemcpyHostToDevice, s), "stage image");
     return;
   }
   const size_t rows_per = std::max<size_t>(1, (size_t)(16u << 20) / std::max<size_t>(width, 1));
@@ -1114,7 +1132,7 @@ void stage_host_image(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t heig
     if (n >= (size_t)tfg_ctx::kSlots) ck(cudaEventSynchronize(ctx->copied[sl]), "event sync");
     uint8_t* slot = static_cast<uint8_t*>(ctx->hslot[sl].p);
     parallel_memcpy(slot, px + r * width, rows * width);
-    ck(cudaMemcpy2DAsync(d_dst + r * dpitch, dpitch, slot, width, width, rows, cudaMemcpyHostToDevice, s),
+    ck(copy_rows(d_dst + r * dpitch, dpitch, slot, width, width, rows, cudaMemcpyHostToDevice, s),
        "stage image");
     ck(cudaEventRecord(ctx->copied[sl], s), "event record");
   }
@@ -1413,7 +1431,7 @@ int glcm_impl_locked(tfg_ctx* ctx, const uint8_t* px, size_t width, size_t heigh
       dstride = dpitch * height;
       uint8_t* buf = static_cast<uint8_t*>(ctx->img.get(dstride * n_bands + 64));
       for (size_t b = 0; b < n_bands; ++b)
-        ck(cudaMemcpy2DAsync(buf + b * dstride, dpitch, px + b * band_stride, pitch, width, height,
+        ck(copy_rows(buf + b * dstride, dpitch, px + b * band_stride, pitch, width, height,
                              dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s),
            "stage image");
       d_img = buf;
