@@ -820,6 +820,7 @@ def run_engine(args, wl):
                 allk[i * rows_e2e * W:(i + 1) * rows_e2e * W].copy_(src)
             pinned = {"all": allk}
         first = next(iter(pinned.values()))
+        in_kind = lib.tfg_memory_kind(C.c_void_p(first.data_ptr()))  # 1 = pinned (tfg_memory_kind)
         probe = torch.empty(first.numel(), dtype=torch.uint8, device="cuda")
         h2d_gbs = []
         for _ in range(3):
@@ -900,7 +901,10 @@ def run_engine(args, wl):
                       ", one call = one continuous Scheme-3 copy/vote stream pipeline, counts to host" +
                       (", + NCCL reduce" if dist else ""),
                "pinned_h2d_GBps": max(h2d_gbs), "ms_per_step": e2e_s * 1e3,
-               "h2d_bound_ms_per_step": h2d / (max(h2d_gbs) * 1e9) * 1e3}
+               "h2d_bound_ms_per_step": h2d / (max(h2d_gbs) * 1e9) * 1e3,
+               "spread_ms": [min(samples) * 1e3, max(samples) * 1e3],
+               "host_memory_kind": {"input": in_kind,
+                                    "counts": lib.tfg_memory_kind(out_host.ctypes.data_as(C.c_void_p))}}
 
     # Secondary end-to-end line through the C++ drop-in's hottest call, in the
     # reference CLI's calling convention (R/tools/texforge.cpp:218-236): a
