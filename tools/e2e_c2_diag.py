@@ -40,6 +40,10 @@ def main():
     res = {}
     res["shard_jobs"] = dist(lambda: eng.shard_jobs(px, w, w, w, jobs, n_bands=2, band_stride=w * w, out=out))
     res["shard_jobs_no_rows"] = dist(lambda: eng.shard_jobs(px, w, w, 0, jobs, n_bands=2, band_stride=w * w, out=out))
+    def with_sync():
+        eng.shard_jobs(px, w, w, w, jobs, n_bands=2, band_stride=w * w, out=out)
+        torch.cuda.synchronize()
+    res["shard_jobs_then_device_sync"] = dist(with_sync)
     out_np = np.zeros(out.size, dtype=np.uint64)
     res["shard_jobs_pageable_out"] = dist(lambda: eng.shard_jobs(px, w, w, w, jobs, n_bands=2, band_stride=w * w,
                                                                  out=out_np))
