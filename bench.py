@@ -142,7 +142,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.sm_max, "reasons": ["unsampled"]}
         sm = [float(s[0]) for s in self.samples]
         reasons = sorted({name for _, m in self.samples for bit, name in self.REASONS.items() if m & bit})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.sm_max, "reasons": reasons,
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": self.sm_max, "reasons": reasons,
                 "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
@@ -882,11 +882,12 @@ def run_engine(args, wl):
         if first < 0.01:
             n_e2e = max(n_e2e, 30)
         samples = []
-        for _ in range(n_e2e):
-            t = time.perf_counter()
-            e2e_step()
-            torch.cuda.synchronize()
-            samples.append(time.perf_counter() - t)
+        with ClockSampler(local) as e2e_clocks:  # short steps leave the GPU mostly idle (clock governor)
+            for _ in range(n_e2e):
+                t = time.perf_counter()
+                e2e_step()
+                torch.cuda.synchronize()
+                samples.append(time.perf_counter() - t)
         e2e_s = statistics.median(samples)
         if dist:
             tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
@@ -902,7 +903,7 @@ def run_engine(args, wl):
                       (", + NCCL reduce" if dist else ""),
                "pinned_h2d_GBps": max(h2d_gbs), "ms_per_step": e2e_s * 1e3,
                "h2d_bound_ms_per_step": h2d / (max(h2d_gbs) * 1e9) * 1e3,
-               "spread_ms": [min(samples) * 1e3, max(samples) * 1e3],
+               "spread_ms": [min(samples) * 1e3, max(samples) * 1e3], "clocks": e2e_clocks.summary(),
                "host_memory_kind": {"input": in_kind,
                                     "counts": lib.tfg_memory_kind(out_host.ctypes.data_as(C.c_void_p))}}
 
