@@ -38,6 +38,35 @@ def main():
     out = torch.zeros(2 * sum(j[0] ** 2 for j in jobs), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
     px = allk.numpy()
     res = {}
+    mode = sys.argv[1] if len(sys.argv) > 1 else ""
+    if "graph" in mode:  # the bench's device-resident leg first: one step captured and replayed
+        import ctypes as C
+        from paper_1710_06189_b200 import _lib as Lb
+        lib = Lb.load()
+        dev = allk.cuda()
+        acc = torch.zeros(2 * sum(j[0] ** 2 for j in jobs), dtype=torch.int64, device="cuda")
+        n = len(jobs)
+        ll = (C.c_int * n)(*[j[0] for j in jobs])
+        dd = (C.c_int * n)(*[j[1] for j in jobs])
+        aa = (C.c_int * n)(*[j[2] for j in jobs])
+        st = torch.cuda.Stream()
+
+        def step():
+            Lb.check(lib.tfg_glcm_jobs_async(eng.handle, C.c_void_p(dev.data_ptr()), w, w, w, w * w, 2, w, 256, ll, dd,
+                                             aa, n, 0, C.c_void_p(acc.data_ptr()), C.c_void_p(st.cuda_stream)))
+        with torch.cuda.stream(st):
+            step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            step()
+        for _ in range(20):
+            g.replay()
+        torch.cuda.synchronize()
+    if "engine2" in mode:
+        eng2 = tf.Engine(0)
+        eng2.synth_noise_device(w, 64, 1)
+        torch.cuda.synchronize()
     res["shard_jobs"] = dist(lambda: eng.shard_jobs(px, w, w, w, jobs, n_bands=2, band_stride=w * w, out=out))
     res["shard_jobs_no_rows"] = dist(lambda: eng.shard_jobs(px, w, w, 0, jobs, n_bands=2, band_stride=w * w, out=out))
     def with_sync():
