@@ -561,6 +561,31 @@ def test_jobs_cooperative_partials(engine, levels, prequant, nb):
                 assert np.array_equal(got[t, b], want), (rep, levels, d, a, b)
 
 
+@pytest.mark.parametrize("levels", [256, 120])
+def test_jobs_ksel_pair_7_8(engine, levels):
+    # 0 deg with 8 <= d < 16: KSEL 7 (d % 16 in 8..11) and 8 (12..15), the
+    # {7, 8} pair of glcm_vote_jobs2_kernel (PACKED16: one launch) and two
+    # one-KSEL launches for COPY1
+    import torch
+    w, h = 1024, 96
+    img = tf.synth_smooth(w, h, 7).pixels
+    dev = torch.from_numpy(img).cuda()
+    dts = [(8, 0), (9, 0), (12, 0), (13, 0), (15, 0)]
+    n = len(dts)
+    lv = (C.c_int * n)(*([levels] * n))
+    dd = (C.c_int * n)(*[d for d, _ in dts])
+    aa = (C.c_int * n)(*[a for _, a in dts])
+    out = torch.zeros(n * levels * levels, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+    before = engine.launches
+    L.check(engine._lib.tfg_glcm_jobs_async(engine.handle, C.c_void_p(dev.data_ptr()), w, h, w, w * h, 1, h, 256,
+                                            lv, dd, aa, n, 0, C.c_void_p(out.data_ptr()), C.c_void_p(s.cuda_stream)))
+    assert engine.launches - before == (1 if levels > 128 else 2)
+    got = out.cpu().numpy().view(np.uint64).reshape(n, -1)
+    for t, (d, a) in enumerate(dts):
+        assert np.array_equal(got[t], O.glcm_gray(img, w, h, levels, d, a)), (levels, d)
+
+
 def test_jobs_cooperative_rows_exceed_one_wave(engine):
     # 20 bands x 8 jobs of one KSEL (90 deg) = 160 (job, band) rows > 148 SM
     # slots: the cooperative launch needs every row co-resident, so
