@@ -746,6 +746,8 @@ def run_engine(args, wl):
                 fe0.record(stream)
                 run_step()
                 fe1.record(stream)
+                while not fe1.query():
+                    time.sleep(0.0002)
                 torch.cuda.synchronize()
                 steps_ms += fe0.elapsed_time(fe1)
             ms = steps_ms / args.steps
@@ -754,6 +756,10 @@ def run_engine(args, wl):
             for s in range(args.steps):
                 run_step()
             end.record(stream)
+            # wait by polling (sleep releases the GIL, so the clock sampler
+            # thread runs during the timed region); the time is the events'
+            while not end.query():
+                time.sleep(0.0005)
             torch.cuda.synchronize()
             ms = start.elapsed_time(end) / args.steps
     gpu_launches = graph_launches * args.steps if graph is not None else eng.launches - l0
