@@ -202,10 +202,29 @@ __device__ __forceinline__ uint32_t vote_addr(uint32_t hb, uint32_t x) {
   else return (x & 0x7fffu) * 4u + hb;
 }
 
-// PACKED16 increment for pixel j of word Q: 1 or 0x10000 by the sign of the
-// reference byte (b >= 128 -> high half): PRMT sign-replicate + 1.
+#ifndef TFG_PACKED_NEG
+#define TFG_PACKED_NEG 1
+#endif
+// PACKED16 increment for pixel j of word Q (b = reference byte).
+// TFG_PACKED_NEG (default): ONE PRMT builds 1 (b < 128) or 0xFFFF0001
+// (b >= 128; byte 0 from the constant 1, bytes 2-3 the sign of b), so a word
+// holds N - 65536 n_hi: low half = N = all votes of its two cells, high half
+// = -n_hi mod 2^16 (packed_decode). Otherwise: 1 or 0x10000 (PRMT + add).
 __device__ __forceinline__ uint32_t packed_inc(uint32_t Q, int j) {
+#if TFG_PACKED_NEG
+  return prmt(Q, 1u, 0x0054u | ((8u + j) << 8) | ((8u + j) << 12));
+#else
   return prmt(Q, 0u, 0x4400u | ((8u + j) << 4) | (8u + j)) + 1u;
+#endif
+}
+// a PACKED16 word as (n_lo | n_hi << 16)
+__device__ __forceinline__ uint32_t packed_decode(uint32_t w) {
+#if TFG_PACKED_NEG
+  const uint32_t nhi = (0u - (w >> 16)) & 0xFFFFu;
+  return ((w & 0xFFFFu) - nhi) | (nhi << 16);
+#else
+  return w;
+#endif
 }
 
 // PACKED16 overflow rule (exact, no barriers, no per-vote ownership test).
@@ -219,16 +238,26 @@ __device__ __forceinline__ uint32_t packed_inc(uint32_t Q, int j) {
 // that votes on it sees bit 15 and drains before its next item, and a warp
 // adds <= 512 to one field per item (32 lanes x 16), so before the first
 // drain lands the field stays < 2^15 + 32 * 512 + 512 < 2^16.
+// TFG_PACKED_NEG: the low half counts both cells, so it alone carries the
+// drain bit, and a drain takes the whole word (atom.exch 0) and decodes it;
+// the bound is the same (N < 2^15 + 33 * 512).
 constexpr uint32_t kDrainBit = 0x80008000u;
+constexpr uint32_t kPackedDrainBit = TFG_PACKED_NEG ? 0x00008000u : 0x80008000u;
 static_assert(32768u + (kThreads / 32 + 1) * 512u < 65536u, "PACKED16 field bound");
 
 // Drains one PACKED16 word whose cell is x = a + 256 b (b's top bit selects
 // the half; the word holds cells (a, b&127) and (a, (b&127)+128)).
 __device__ __forceinline__ void packed_drain(uint32_t addr, uint32_t x, unsigned long long* glcm, uint32_t L) {
   uint32_t old;
-  asm volatile("atom.shared.and.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(0x07FF07FFu) : "memory");
   const uint32_t a = x & 0xFFu, b = (x >> 8) & 0x7Fu;
+#if TFG_PACKED_NEG
+  asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(0u) : "memory");
+  const uint32_t dec = packed_decode(old);
+  const uint32_t lo = dec & 0xFFFFu, hi = dec >> 16;
+#else
+  asm volatile("atom.shared.and.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(0x07FF07FFu) : "memory");
   const uint32_t lo = old & 0xF800u, hi = (old >> 16) & 0xF800u;
+#endif
   if (lo) atomicAdd(glcm + b * L + a, (unsigned long long)lo);
   if (hi) atomicAdd(glcm + (b + 128u) * L + a, (unsigned long long)hi);
 }
@@ -271,7 +300,7 @@ __device__ __noinline__ void vote_masked(uint32_t hb, uint32_t P0, uint32_t P1, 
   for (int k = 0; k < 16; ++k)
     if (mask & (1u << k)) flag |= emit<STRAT>(hb, P[k >> 2], Q[k >> 2], k & 3, 1u);
   if constexpr (STRAT == S_PACKED16) {
-    if (flag & kDrainBit) packed_drain_item(hb, P0, P1, P2, P3, Q0, Q1, Q2, Q3, mask, glcm, L);
+    if (flag & kPackedDrainBit) packed_drain_item(hb, P0, P1, P2, P3, Q0, Q1, Q2, Q3, mask, glcm, L);
   }
 }
 
@@ -287,7 +316,7 @@ __device__ __forceinline__ void packed_vote16(uint32_t hb, const uint32_t (&P)[4
 #pragma unroll
     for (int j = 0; j < 4; ++j) flag |= atom_smem(hb + pair_x(P[i], Qm, j) * 4u, packed_inc(Q[i], j));
   }
-  if (flag & kDrainBit) packed_drain_item(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], 0xFFFFu, glcm, L);
+  if (flag & kPackedDrainBit) packed_drain_item(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], 0xFFFFu, glcm, L);
 }
 
 // ---- S_P16X16 (L <= 64): 16 copies of packed u16 counters. Lanes l and
@@ -384,7 +413,7 @@ __device__ __forceinline__ bool vote16(uint32_t hb, const uint32_t (&P)[4], cons
       if (diff == 0) {
         const uint32_t old = emit<STRAT>(hb, P[0], Q[0], 0, 16u);
         if constexpr (STRAT == S_PACKED16) {
-          if (old & kDrainBit) packed_drain_item(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], 1u, glcm, L);
+          if (old & kPackedDrainBit) packed_drain_item(hb, P[0], P[1], P[2], P[3], Q[0], Q[1], Q[2], Q[3], 1u, glcm, L);
         }
         return true;
       }
@@ -1293,7 +1322,10 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
     if constexpr (STRAT == S_PACKED16) {
       uint4* dst = reinterpret_cast<uint4*>(p.partials + ((size_t)unit * gridDim.x + blockIdx.x) * (size_t)p.hist_words);
       const uint4* src = reinterpret_cast<const uint4*>(hist);
-      for (int i = tid; i < (p.hist_words >> 2); i += kThreads) dst[i] = src[i];
+      for (int i = tid; i < (p.hist_words >> 2); i += kThreads) {
+        const uint4 v = src[i];
+        dst[i] = make_uint4(packed_decode(v.x), packed_decode(v.y), packed_decode(v.z), packed_decode(v.w));
+      }
     } else {
       uint32_t* part = p.partials + ((size_t)unit * gridDim.x + blockIdx.x) * (size_t)cells;
       constexpr int RC = strat_copies(STRAT);
