@@ -31,7 +31,7 @@
 // reference bytes are pre-scaled so that ONE byte permute (PRMT) of an anchor
 // word and a reference word gives a pixel pair's shared-memory offset, then
 // one IMAD adds the lane's copy base and one red.shared.add (ATOMS.POPC.INC)
-// casts the vote; 6 for the packed-u16 L=256 layout (kDrainBit).
+// casts the vote; 5 for the packed-u16 L=256 layout (packed_inc, kPackedDrainBit).
 //
 // Measured A/B variants kept behind flags: TFG_TMA (TMA-staged
 // main pass), S_P16X16 (16 bank-pair copies for L <= 64), TFG_LDG_MODE
@@ -66,8 +66,8 @@ enum Strat : int {
   S_COPIES8 = 2,   // L <= 64:  8 u32 copies [b + 64a][lane%8]; P = 4b, Q = a, addr = 8x + 4 (lane%8)
   S_COPY1 = 3,     // L <= 128: 1 u32 copy [a + 128b]; P = 2a, Q = b, addr = 2x
   S_P16X16 = 5,    // L <= 64: 16 copies of u16 counters, copy = lane & 15 owning banks 2k, 2k+1 (p16x16_*)
-  S_PACKED16 = 4   // L <= 256: 1 copy of u16 counters, cell a + 256b in word (x & 0x7fff), half b >> 7,
-                   //           drained to the u64 cells past 2^15 (kDrainBit)
+  S_PACKED16 = 4   // L <= 256: 1 copy of u16 counters, cell a + 256b in word (x & 0x7fff), half b >> 7
+                   //           (word = N - 65536 n_hi, packed_inc), drained past 2^15 (kPackedDrainBit)
 };
 
 __host__ __device__ constexpr int strat_scale(int s) {  // log2 of the P-byte scale
@@ -305,7 +305,7 @@ __device__ __noinline__ void vote_masked(uint32_t hb, uint32_t P0, uint32_t P1, 
 }
 
 // The 16 PACKED16 votes of an unmasked item (returning atomics, then the
-// drain rule of kDrainBit). Reference bytes with the half bit cleared: PRMT
+// drain rule of kPackedDrainBit). Reference bytes with the half bit cleared: PRMT
 // then yields the word index a + 256 (b & 127) directly (no per-vote mask).
 __device__ __forceinline__ void packed_vote16(uint32_t hb, const uint32_t (&P)[4], const uint32_t (&Q)[4],
                                               unsigned long long* glcm, uint32_t L) {
@@ -756,7 +756,7 @@ __device__ __forceinline__ void reduce_partials_slice(const VoteParams& p, uint3
 //    plus a per-lane row-wrap select.
 //  * edge pass — the first and last segment of every row (or every segment
 //    of a narrow image), with per-lane guarded loads and valid-anchor masks.
-// There is no barrier in either loop (PACKED16 included: see kDrainBit).
+// There is no barrier in either loop (PACKED16 included: see kPackedDrainBit).
 // vote_cta: the work of CTA `cta` of band `band_idx` (glcm_vote_kernel: the
 // block's x and y; glcm_vote_jobs_kernel: one job's share of the grid).
 template <int QUANT, int STRAT, int KSEL>
