@@ -790,7 +790,13 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
   const uint32_t nch = (uint32_t)p.nch;
   const uint32_t ni = (uint32_t)p.ni;
 
-  bool rle = true;  // PACKED16 run-length check; re-sampled every 8th item when it stops paying
+#ifndef TFG_RLE_PERIOD
+#define TFG_RLE_PERIOD 8  // items between re-samples once the check stops paying (power of 2)
+#endif
+#ifndef TFG_RLE_MIN
+#define TFG_RLE_MIN 4  // uniform lanes of a warp-item for the check to keep paying
+#endif
+  bool rle = true;  // PACKED16 run-length check; re-sampled every TFG_RLE_PERIOD-th item when it stops paying
   uint32_t nb = 0;
   // Votes one item (16 pairs, or the pairs in `mask`).
   // S_P16X16: quantised anchor / reference words of an item
@@ -812,9 +818,9 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
     uint32_t P[4], Q[4];
     item_words<QUANT, STRAT, KSEL>(p, cur, P, Q);
     if constexpr (STRAT == S_PACKED16) {
-      const bool check = rle || (nb & 7) == 0;
+      const bool check = rle || (nb & (TFG_RLE_PERIOD - 1)) == 0;
       const bool hit = vote16<STRAT>(hb, P, Q, cur.mask, check, glcm, L);
-      if (check) rle = __popc(__ballot_sync(0xffffffffu, hit)) >= 4;
+      if (check) rle = __popc(__ballot_sync(0xffffffffu, hit)) >= TFG_RLE_MIN;
       ++nb;
     } else if (cur.mask == 0xFFFFu) {
       // conflict-free (COPIES*) or hardware-aggregated (COPY1: POPC.INC) layouts
@@ -836,9 +842,9 @@ __device__ __forceinline__ void vote_cta(const VoteParams& p, const uint32_t cta
     uint32_t P[4], Q[4];
     item_words<QUANT, STRAT, KSEL>(p, cur, P, Q);
     if constexpr (STRAT == S_PACKED16) {
-      const bool check = rle || (nb & 7) == 0;
+      const bool check = rle || (nb & (TFG_RLE_PERIOD - 1)) == 0;
       const bool hit = vote16<STRAT>(hb, P, Q, 0xFFFFu, check, glcm, L);
-      if (check) rle = __popc(__ballot_sync(0xffffffffu, hit)) >= 4;
+      if (check) rle = __popc(__ballot_sync(0xffffffffu, hit)) >= TFG_RLE_MIN;
       ++nb;
     } else {
 #pragma unroll
