@@ -710,12 +710,13 @@ def run_engine(args, wl):
     if dist:
         dist.barrier()
 
-    # Launch-bound steps (many short vote launches) replay ONE CUDA graph of
-    # the step, so the timed region measures the device, not the host's
-    # launch rate. Not for cooperative launches (L > 64) or steps with an NCCL reduce.
+    # The step is replayed as ONE CUDA graph, so the timed region measures the
+    # device, not the host's launch rate or the gaps between launches
+    # (cooperative L > 64 launches capture too: c3 +0.7%). Not for steps with
+    # an NCCL reduce. TFG_BENCH_GRAPH=0: eager engine calls.
     graph, graph_launches = None, 0
     nccl_step = dist is not None and plan.layout.startswith("rows")
-    if not nccl_step and max(plan.levels_list) <= 64 and os.environ.get("TFG_BENCH_GRAPH", "1") != "0":
+    if not nccl_step and os.environ.get("TFG_BENCH_GRAPH", "1") != "0":
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)
         graph = torch.cuda.CUDAGraph()
